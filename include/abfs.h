@@ -1,0 +1,193 @@
+/*
+ * abfs.h -- C ABI of the B200-native tree-switched level-synchronous BFS
+ * engine (libabfs.so, built from paper_1708_01159_b200/csrc/).
+ *
+ * The reference (/root/reference/pkg/src/adaptive_bfs/, pure Python + numpy)
+ * has no FFI: its operator API is the Python callables listed beside each
+ * entry point below ("replaces ...").  The Python package
+ * paper_1708_01159_b200 binds this header with ctypes and re-exposes the
+ * reference names and signatures; INTEGRATION.md shows the binding a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *   - every call returns an abfs_status; abfs_last_error() gives the
+ *     thread-local message of the last failure (mapped to ValueError with the
+ *     reference's text by the Python layer);
+ *   - plain pointers + sizes only; "host" pointers are ordinary CPU memory,
+ *     the engine owns all device memory;
+ *   - one CUDA stream per traversal (settable), calls on one traversal are not
+ *     reentrant (same rule as bfs_full on one depth array);
+ *   - depths are int32 with INF = 2^31-1 (kernels.py:30-31).
+ */
+#ifndef ABFS_H
+#define ABFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ABFS_API __attribute__((visibility("default")))
+#else
+#define ABFS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ABFS_OK = 0,
+    ABFS_EINVAL = 1,    /* invalid argument (root/chunk/kernel/variant/...)   */
+    ABFS_ECUDA = 2,     /* CUDA runtime error                                 */
+    ABFS_ENCCL = 3,     /* reserved: multi-GPU exchange error                 */
+    ABFS_ENOMEM = 4,    /* device or host allocation failed                   */
+    ABFS_EFEATURE = 5   /* invalid runtime feature state (features.py:103-110)*/
+} abfs_status;
+
+#define ABFS_INF_DEPTH 2147483647
+#define ABFS_LEAF_UNKNOWN 254   /* tree.py:25 */
+#define ABFS_NOT_A_LEAF 255     /* tree.py:26 */
+#define ABFS_N_FEATURES 24      /* features.py:25-35 canonical order */
+
+/* KernelId (kernels.py:40-47) and CountVariant (kernels.py:50-55). */
+enum { ABFS_EDGE_LIST = 0, ABFS_REV_EDGE_LIST = 1, ABFS_VERTEX_PUSH = 2,
+       ABFS_VERTEX_PULL = 3, ABFS_VERTEX_PUSH_WARP = 4 };
+enum { ABFS_DIRECT_ATOMIC = 0, ABFS_GROUP_REDUCE = 1, ABFS_TWO_LEVEL_REDUCE = 2 };
+
+typedef struct abfs_graph abfs_graph;          /* device-resident Graph      */
+typedef struct abfs_traversal abfs_traversal;  /* device depth/frontier state */
+
+/* FlatTree (tree.py:303-359) in array form.  selection[i] is the canonical
+ * FEATURE_NAMES index of the tree's i-th selected feature; features[node]
+ * indexes into the selection (tree.py:332-339). */
+typedef struct {
+    uint32_t node_count;
+    uint32_t n_selection;
+    const uint16_t *selection;
+    const uint16_t *features;
+    const double *thresholds;
+    const uint32_t *lefts;
+    const uint32_t *rights;
+    const uint8_t *leaf_classes;
+} abfs_tree;
+
+/* One LevelTrace (adaptive.py:51-60) plus engine diagnostics. */
+typedef struct {
+    int64_t level;
+    int32_t kernel;
+    int32_t variant;
+    int32_t fallback;
+    int32_t converted;        /* 1 if a queue<->bitmap conversion ran (switch cost) */
+    uint64_t frontier_size;
+    uint64_t new_count;
+    uint64_t elapsed_ns;      /* CUDA-event time of the level incl. conversion */
+    uint64_t prediction_ns;   /* host feature extraction + tree descent        */
+} abfs_level_record;
+
+ABFS_API const char *abfs_last_error(void);
+ABFS_API int abfs_version(void);
+
+/* ---- graph (graph.py) --------------------------------------------------- */
+
+/* Upload a host combined representation (replaces Graph, graph.py:27-69;
+ * rev_owner (graph.py:57-65) is derived on the device). */
+ABFS_API int abfs_graph_upload(int device, uint64_t n, uint64_t m,
+                      const uint32_t *out_offsets, const uint32_t *destinations,
+                      const uint32_t *origins, const uint32_t *in_offsets,
+                      const uint32_t *sources, abfs_graph **out);
+
+/* Device build_combined from host (src, dst) pairs (replaces
+ * build_combined, graph.py:93-134; pairs must be range-checked). */
+ABFS_API int abfs_graph_build(int device, uint64_t n, uint64_t m, const uint32_t *src,
+                     const uint32_t *dst, abfs_graph **out);
+
+/* Device generators, bit-exact to generate_graph (graph.py:211-252):
+ * pcg_state/pcg_inc are numpy default_rng(seed)'s PCG64 words (hi, lo).
+ * symmetrize=1 appends the reversed pairs. */
+ABFS_API int abfs_graph_generate_rmat(int device, uint32_t scale, uint64_t edges,
+                             double a, double b, double c,
+                             const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                             int symmetrize, abfs_graph **out);
+/* uniform-random (graph.py:226-231); n must be a power of two <= 2^32. */
+ABFS_API int abfs_graph_generate_uniform(int device, uint64_t n, uint64_t edges,
+                                const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                                abfs_graph **out);
+/* rows x cols 4-neighbour grid, both directions. */
+ABFS_API int abfs_graph_generate_mesh(int device, uint32_t rows, uint32_t cols,
+                             abfs_graph **out);
+
+ABFS_API int abfs_graph_info(const abfs_graph *g, uint64_t *n, uint64_t *m, int *device);
+/* Copy arrays back to host; any pointer may be NULL (skipped). */
+ABFS_API int abfs_graph_download(const abfs_graph *g, uint32_t *out_offsets,
+                        uint32_t *destinations, uint32_t *origins,
+                        uint32_t *in_offsets, uint32_t *sources, uint32_t *rev_owner);
+ABFS_API void abfs_graph_destroy(abfs_graph *g);
+
+/* ---- traversal state ---------------------------------------------------- */
+
+ABFS_API int abfs_traversal_create(abfs_graph *g, abfs_traversal **out);
+ABFS_API void abfs_traversal_destroy(abfs_traversal *t);
+/* Use an external cudaStream_t (NULL = engine-owned stream). */
+ABFS_API int abfs_traversal_set_stream(abfs_traversal *t, void *cuda_stream);
+
+/* init_depths on the device (replaces init_depths, kernels.py:134-140). */
+ABFS_API int abfs_init_depths(abfs_traversal *t, int64_t root);
+/* Arbitrary caller depths (run_level contract, tests/test_kernels.py:209-236);
+ * the next level rebuilds its frontier from the depth array. */
+ABFS_API int abfs_load_depths(abfs_traversal *t, const int32_t *host_depths);
+ABFS_API int abfs_read_depths(abfs_traversal *t, int32_t *host_depths);
+
+/* One level on the device-resident state (replaces run_level,
+ * kernels.py:340-353): kernel/variant/chunk as in the reference; one small
+ * readback.  new_count = INF->level+1 transitions. */
+ABFS_API int abfs_level(abfs_traversal *t, int64_t level, int kernel, int variant,
+               int64_t chunk_size, uint64_t *new_count, uint64_t *elapsed_ns);
+
+/* run_level on a caller-owned HOST depth array, mutated in place
+ * (H2D, level, D2H). */
+ABFS_API int abfs_run_level(abfs_traversal *t, int32_t *host_depths, int64_t level,
+                   int kernel, int variant, int64_t chunk_size,
+                   uint64_t *new_count, uint64_t *elapsed_ns);
+
+/* bfs_full (kernels.py:356-371).  counts/elapsed receive one entry per
+ * executed level (terminating zero level included) up to cap; depths_out may
+ * be NULL (depths stay on the device). */
+ABFS_API int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int variant,
+                  int64_t chunk_size, int32_t *depths_out, uint64_t *counts,
+                  uint64_t *elapsed, size_t cap, size_t *n_levels);
+
+/* adaptive_bfs with a FlatTree model (adaptive.py:83-129): per level the
+ * device produces the new count, the host evaluates the tree on the
+ * reference's float64 features (features.py:98-121; static24 holds the 24
+ * canonical features, slots 2..5 ignored), then launches the chosen pair. */
+ABFS_API int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree *tree,
+                      const double *static24, int64_t chunk_size,
+                      int32_t *depths_out, abfs_level_record *records,
+                      size_t cap, size_t *n_levels);
+
+/* Total device time (ns) of the last abfs_bfs_full/abfs_adaptive_bfs call,
+ * from after init_depths to the final count readback. */
+ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
+
+/* Sum over reached vertices of out-degree (GTEPS numerator basis). */
+ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices);
+
+/* ---- helpers ------------------------------------------------------------ */
+
+/* aggregate_count (kernels.py:143-170) on the device with the three
+ * reduction shapes: DIRECT = 1 atomic/item, GROUP = warp reduce + 1
+ * atomic/warp, TWO_LEVEL = warp + CTA reduce + 1 atomic/CTA. */
+ABFS_API int abfs_aggregate_count(int device, const int64_t *host_counts, size_t n,
+                         int variant, int64_t *total);
+
+/* FlatTree.predict_one (tree.py:332-339) on a projected vector. */
+ABFS_API int abfs_tree_predict(const abfs_tree *tree, const double *projected, int *leaf_class);
+
+/* extract_runtime_features (features.py:98-121) into out24 (canonical). */
+ABFS_API int abfs_features(const double *static24, uint64_t frontier_abs,
+                  uint64_t discovered_abs, double *out24);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABFS_H */

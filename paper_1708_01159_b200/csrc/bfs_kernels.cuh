@@ -1,0 +1,568 @@
+// bfs_kernels.cuh -- the 5 level strategies x 3 count epilogues, the
+// queue<->bitmap frontier conversions and the state kernels (sm_100a).
+//
+// Semantics (all strategies; kernels.py:177-193):
+//   * a level may only lower a depth to level+1;
+//   * new_count = number of INF -> level+1 transitions (exactly once each);
+//   * top-down strategies (edge, rev-edge, push, push-warp) lower any depth
+//     > level+1 reached from a frontier vertex; pull only touches INF vertices.
+//
+// Frontier state on the device (the reference's implicit `depth == level`):
+//   visited  u32 bitmap   bit v <=> depth[v] != INF (maintained exactly)
+//   fbm      u32 bitmap   current frontier (depth == level)   [bitmap form]
+//   q        u32 queue    current frontier vertex ids           [queue form]
+// Top-down kernels emit the next frontier as a queue, pull emits a bitmap;
+// the engine converts between forms only when the next kernel needs the
+// other one (that conversion is the switching overhead).
+//
+// "Consistent" state (every finite depth <= level+1, which a BFS from
+// init_depths always satisfies) lets a claim be a single atomicOr on the
+// L2-resident visited bitmap followed by a plain depth store.  Arbitrary
+// caller depth arrays (run_level contract) set ctr->inconsistent and claims
+// fall back to atomicMin on the depth array, which reproduces _claim's
+// "lower to level+1, count only INF transitions" rule exactly.
+#pragma once
+
+#include "common.cuh"
+
+namespace abfs {
+
+// Device counters.  Slots rotate per level call so that no separate zeroing
+// launch is needed: call c appends into slot c%3 and zeroes slot (c+1)%3.
+struct Ctr {
+    unsigned int qlen[3];
+    unsigned int units[3];
+    unsigned long long count[3];
+    unsigned int cq;             // bitmap->queue compaction cursor
+    unsigned int inconsistent;   // 1 if some finite depth > level+1 (prepare)
+    unsigned long long fcount;   // frontier size found by prepare
+    unsigned long long reached_edges;
+    unsigned long long reached_vertices;
+};
+
+struct LevelCtx {
+    int32_t *depth;
+    uint32_t *visited;
+    const uint32_t *fbm;         // current frontier bitmap (read-only here)
+    uint32_t *q_next;            // next frontier queue (top-down)
+    unsigned int *q_tail;        // = &ctr->qlen[out]
+    unsigned long long *count;   // = &ctr->count[out] (pull)
+    const unsigned int *inconsistent;
+    Ctr *ctr;
+    int zero_slot;
+    int32_t level;
+    int32_t lvl1;
+};
+
+constexpr int kBlock = 256;
+constexpr int kQBuf = 2048;          // TWO_LEVEL CTA-local queue buffer
+constexpr int kEdgeTile = kBlock * 8; // edge slots per CTA (2 x uint4 per thread)
+constexpr uint32_t kHeavy = 2048;    // push-warp: degree above -> CTA units
+constexpr uint32_t kUnit = 4096;     // edges per CTA work unit
+
+__device__ __forceinline__ void zero_slot(const LevelCtx &c) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c.ctr->qlen[c.zero_slot] = 0;
+        c.ctr->units[c.zero_slot] = 0;
+        c.ctr->count[c.zero_slot] = 0;
+        c.ctr->cq = 0;
+    }
+}
+
+__device__ __forceinline__ bool in_bitmap(const uint32_t *bm, uint32_t v) {
+    return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Could claiming v change anything?  (cheap filter before the atomic)
+__device__ __forceinline__ bool claim_possible(const LevelCtx &c, uint32_t v, bool consistent) {
+    if (consistent) return !((c.visited[v >> 5] >> (v & 31)) & 1u);
+    return c.depth[v] > c.lvl1;
+}
+
+// _claim (kernels.py:177-193) for one candidate; true iff this thread won
+// the INF -> level+1 transition of v.
+__device__ __forceinline__ bool claim(const LevelCtx &c, uint32_t v, bool consistent) {
+    const uint32_t bit = 1u << (v & 31);
+    uint32_t *w = c.visited + (v >> 5);
+    if (consistent) {
+        if (*w & bit) return false;
+        const uint32_t old = atomicOr(w, bit);
+        if (old & bit) return false;
+        c.depth[v] = c.lvl1;
+        return true;
+    }
+    if (c.depth[v] <= c.lvl1) return false;
+    const int32_t old = atomicMin(c.depth + v, c.lvl1);
+    if (old != kInf) return false;
+    atomicOr(w, bit);
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Count epilogues (aggregate_count kernels.py:143-170).
+// QEmit: winners append to the next queue; the append cursor IS the count.
+//   VAR 0 DIRECT_ATOMIC    one global atomic per discovery
+//   VAR 1 GROUP_REDUCE     warp ballot/popc, one global atomic per warp
+//   VAR 2 TWO_LEVEL_REDUCE warp ballot -> CTA shared-memory queue, one
+//                          global atomic per CTA (coalesced flush)
+// emit() must be called by all 32 lanes of a warp together.
+// ---------------------------------------------------------------------------
+struct SmemQ {
+    unsigned int n;
+    unsigned int fail;
+    unsigned int base;
+    uint32_t buf[kQBuf];
+};
+
+template <int VAR>
+struct QEmit {
+    SmemQ *s;
+    uint32_t *q;
+    unsigned int *tail;
+
+    __device__ __forceinline__ QEmit(SmemQ *sm, uint32_t *qq, unsigned int *t)
+        : s(sm), q(qq), tail(t) {
+        if (VAR == 2) {
+            if (threadIdx.x == 0) { s->n = 0; s->fail = 0xffffffffu; }
+            __syncthreads();
+        }
+    }
+
+    __device__ __forceinline__ void emit(bool won, uint32_t v) {
+        if (VAR == 0) {
+            if (won) q[atomicAdd(tail, 1u)] = v;
+            return;
+        }
+        const unsigned mask = __ballot_sync(kFull, won);
+        if (!mask) return;
+        const unsigned lane = lane_id();
+        const int leader = __ffs(mask) - 1;
+        const unsigned cnt = __popc(mask);
+        const unsigned rank = __popc(mask & ((1u << lane) - 1u));
+        if (VAR == 1) {
+            unsigned b = 0;
+            if (lane == (unsigned)leader) b = atomicAdd(tail, cnt);
+            b = __shfl_sync(kFull, b, leader);
+            if (won) q[b + rank] = v;
+            return;
+        }
+        unsigned sb = 0;
+        if (lane == (unsigned)leader) sb = atomicAdd(&s->n, cnt);
+        sb = __shfl_sync(kFull, sb, leader);
+        if (sb + cnt <= (unsigned)kQBuf) {
+            if (won) s->buf[sb + rank] = v;
+        } else {  // CTA buffer full: this warp batch goes straight to global
+            unsigned b = 0;
+            if (lane == (unsigned)leader) {
+                atomicMin(&s->fail, sb);
+                b = atomicAdd(tail, cnt);
+            }
+            b = __shfl_sync(kFull, b, leader);
+            if (won) q[b + rank] = v;
+        }
+    }
+
+    // Must be reached by every thread of the CTA.
+    __device__ __forceinline__ void finish() {
+        if (VAR != 2) return;
+        __syncthreads();
+        const unsigned n = min(s->n, s->fail);
+        if (threadIdx.x == 0) s->base = n ? atomicAdd(tail, n) : 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x) q[s->base + i] = s->buf[i];
+    }
+};
+
+// Count-only epilogue (pull): same three shapes over a warp's found mask.
+template <int VAR>
+struct CEmit {
+    unsigned int *sn;
+    unsigned long long *count;
+
+    __device__ __forceinline__ CEmit(unsigned int *smem_n, unsigned long long *c)
+        : sn(smem_n), count(c) {
+        if (VAR == 2) {
+            if (threadIdx.x == 0) *sn = 0;
+            __syncthreads();
+        }
+    }
+
+    __device__ __forceinline__ void add(unsigned mask) {  // warp-uniform mask
+        if (VAR == 0) {
+            if ((mask >> lane_id()) & 1u) atomicAdd(count, 1ull);
+        } else if (mask && lane_id() == 0) {
+            if (VAR == 1) atomicAdd(count, (unsigned long long)__popc(mask));
+            else atomicAdd(sn, (unsigned)__popc(mask));
+        }
+    }
+
+    __device__ __forceinline__ void finish() {
+        if (VAR != 2) return;
+        __syncthreads();
+        if (threadIdx.x == 0 && *sn) atomicAdd(count, (unsigned long long)*sn);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// EDGE_LIST (run_level_edge_list + _relax_from_edges, kernels.py:196-219):
+// one item per forward slot e; active iff origins[e] is in the frontier;
+// relax destinations[e].  Origins stream with 128-bit evict-first loads;
+// destinations are gathered only for active slots.
+// REV_EDGE_LIST (kernels.py:222-231): item per reverse slot f, head
+// sources[f], tail rev_owner[f].  The sorted tail stream is read first so
+// that sources[f] is gathered only when the claim could have an effect.
+// ---------------------------------------------------------------------------
+template <int VAR, bool REV>
+__global__ void __launch_bounds__(kBlock)
+k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
+       const uint32_t *__restrict__ gather_arr, uint64_t m) {
+    __shared__ SmemQ sq;
+    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
+    zero_slot(c);
+    const bool consistent = (*c.inconsistent == 0);
+    const uint64_t tile = (uint64_t)blockIdx.x * kEdgeTile;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+        uint32_t s4[4];
+        if (e + 4 <= m) {
+            const uint4 t = __ldcs(reinterpret_cast<const uint4 *>(stream_arr + e));
+            s4[0] = t.x; s4[1] = t.y; s4[2] = t.z; s4[3] = t.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s4[k] = (e + k < m) ? stream_arr[e + k] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            bool won = false;
+            uint32_t v = 0;
+            if (e + k < m) {
+                if (!REV) {
+                    if (in_bitmap(c.fbm, s4[k])) {
+                        v = __ldg(gather_arr + e + k);
+                        won = claim(c, v, consistent);
+                    }
+                } else {
+                    v = s4[k];
+                    if (claim_possible(c, v, consistent) &&
+                        in_bitmap(c.fbm, __ldg(gather_arr + e + k)))
+                        won = claim(c, v, consistent);
+                }
+            }
+            em.emit(won, v);
+        }
+    }
+    em.finish();
+}
+
+// ---------------------------------------------------------------------------
+// VERTEX_PUSH (run_level_vertex_push + _push_block, kernels.py:234-267):
+// one thread per frontier vertex walks its out-adjacency in order.
+// ---------------------------------------------------------------------------
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
+       const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
+    __shared__ SmemQ sq;
+    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
+    zero_slot(c);
+    const bool consistent = (*c.inconsistent == 0);
+    for (uint32_t base = blockIdx.x * kBlock; base < F; base += gridDim.x * kBlock) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t j = 0, e = 0;
+        if (i < F) {
+            const uint32_t u = __ldg(q + i);
+            j = __ldg(out_off + u);
+            e = __ldg(out_off + u + 1);
+        }
+        while (__any_sync(kFull, j < e)) {
+            bool won = false;
+            uint32_t v = 0;
+            if (j < e) {
+                v = __ldg(dst + j);
+                ++j;
+                won = claim(c, v, consistent);
+            }
+            em.emit(won, v);
+        }
+    }
+    em.finish();
+}
+
+// ---------------------------------------------------------------------------
+// VERTEX_PUSH_WARP (run_level_push_warp, kernels.py:303-322; virtual-warp
+// method PAPER.md:414-432): a virtual warp of VW lanes owns one frontier
+// vertex at a time and strides its adjacency in VW-wide coalesced chunks.
+// Vertices with degree > kHeavy are split into kUnit-edge CTA work units
+// processed by k_heavy (CTA-centric push), so hubs never serialise a warp.
+// ---------------------------------------------------------------------------
+template <int VAR, int VW>
+__global__ void __launch_bounds__(kBlock)
+k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
+            const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst,
+            uint2 *units, unsigned int *units_tail) {
+    __shared__ SmemQ sq;
+    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
+    zero_slot(c);
+    const bool consistent = (*c.inconsistent == 0);
+    constexpr uint32_t per = 32 / VW;
+    const unsigned lane = lane_id();
+    const uint32_t sub = lane / VW, sl = lane % VW;
+    const uint32_t warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * kBlock) >> 5;
+    for (uint32_t wb = warp * per; wb < F; wb += nwarps * per) {
+        const uint32_t i = wb + sub;
+        uint32_t j = 0, e = 0;
+        if (i < F) {
+            const uint32_t u = __ldg(q + i);
+            const uint32_t b = __ldg(out_off + u), en = __ldg(out_off + u + 1);
+            if (en - b > kHeavy) {
+                if (sl == 0) {
+                    const uint32_t nu = (en - b + kUnit - 1) / kUnit;
+                    const uint32_t s = atomicAdd(units_tail, nu);
+                    for (uint32_t k = 0; k < nu; ++k) units[s + k] = make_uint2(u, k);
+                }
+            } else {
+                j = b + sl;
+                e = en;
+            }
+        }
+        while (__any_sync(kFull, j < e)) {
+            bool won = false;
+            uint32_t v = 0;
+            if (j < e) {
+                v = __ldg(dst + j);
+                j += VW;
+                won = claim(c, v, consistent);
+            }
+            em.emit(won, v);
+        }
+    }
+    em.finish();
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off,
+        const uint32_t *__restrict__ dst, const uint2 *__restrict__ units,
+        const unsigned int *units_tail) {
+    __shared__ SmemQ sq;
+    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
+    const bool consistent = (*c.inconsistent == 0);
+    const unsigned nunits = *units_tail;
+    for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
+        const uint2 un = units[w];
+        const uint32_t b = __ldg(out_off + un.x) + un.y * kUnit;
+        const uint32_t e = min(__ldg(out_off + un.x + 1), b + kUnit);
+        for (uint32_t jb = b; jb < e; jb += kBlock) {
+            const uint32_t j = jb + threadIdx.x;
+            bool won = false;
+            uint32_t v = 0;
+            if (j < e) {
+                v = __ldg(dst + j);
+                won = claim(c, v, consistent);
+            }
+            em.emit(won, v);
+        }
+    }
+    em.finish();
+}
+
+// ---------------------------------------------------------------------------
+// VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): one warp per
+// 32-vertex bitmap word; each unvisited lane scans its in-neighbours in
+// order and stops at the first frontier vertex.  The warp owns its visited
+// and next-frontier words, so both are written without atomics, and every
+// next-frontier word is written (no clearing pass).
+// ---------------------------------------------------------------------------
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
+       uint32_t *__restrict__ fbm_next, uint64_t n, uint64_t words) {
+    __shared__ unsigned int sn;
+    CEmit<VAR> em(&sn, c.count);
+    zero_slot(c);
+    const unsigned lane = lane_id();
+    const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+    for (uint64_t word = warp; word < words; word += nwarps) {
+        const uint32_t vis = c.visited[word];
+        const uint64_t v = word * 32 + lane;
+        const bool cand = v < n && !((vis >> lane) & 1u);
+        unsigned found_mask = 0;
+        if (__any_sync(kFull, cand)) {
+            uint32_t j = 0, e = 0;
+            if (cand) {
+                j = __ldg(in_off + v);
+                e = __ldg(in_off + v + 1);
+            }
+            bool found = false;
+            while (__any_sync(kFull, j < e)) {
+                if (j < e) {
+                    if (in_bitmap(c.fbm, __ldg(src + j))) {
+                        found = true;
+                        j = e;
+                    } else {
+                        ++j;
+                    }
+                }
+            }
+            found_mask = __ballot_sync(kFull, found);
+            if (found) c.depth[v] = c.lvl1;
+        }
+        if (lane == 0) {
+            fbm_next[word] = found_mask;
+            if (found_mask) c.visited[word] = vis | found_mask;
+        }
+        em.add(found_mask);
+    }
+    em.finish();
+}
+
+// ---------------------------------------------------------------------------
+// Frontier conversions (switching overhead).
+// ---------------------------------------------------------------------------
+
+// bitmap -> queue: per-word popc, warp + CTA scan, one atomic per CTA.
+__global__ void __launch_bounds__(kBlock)
+k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
+                  unsigned int *cursor) {
+    __shared__ unsigned warp_tot[kBlock / 32];
+    __shared__ unsigned base;
+    const uint64_t word = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+    uint32_t w = word < words ? fbm[word] : 0u;
+    const unsigned cnt = __popc(w);
+    const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int i = 0; i < kBlock / 32; ++i) {
+            const unsigned t = warp_tot[i];
+            warp_tot[i] = acc;
+            acc += t;
+        }
+        base = acc ? atomicAdd(cursor, acc) : 0u;
+    }
+    __syncthreads();
+    unsigned pos = base + warp_tot[wid] + incl - cnt;
+    while (w) {
+        const int b = __ffs(w) - 1;
+        q[pos++] = (uint32_t)(word * 32 + b);
+        w &= w - 1;
+    }
+}
+
+// queue -> bitmap (bitmap cleared by the caller).
+__global__ void k_queue_to_bitmap(const uint32_t *__restrict__ q, uint32_t F, uint32_t *fbm) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+        const uint32_t v = q[i];
+        atomicOr(fbm + (v >> 5), 1u << (v & 31));
+    }
+}
+
+// init_depths (kernels.py:134-140) + frontier {root} in both forms.
+__global__ void k_init(int32_t *depth, uint32_t *visited, uint32_t *fbm, uint32_t *q,
+                       uint64_t n, uint64_t words, uint32_t root) {
+    const uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (word >= words) return;
+    const uint64_t v0 = word * 32;
+    if (v0 + 32 <= n) {
+        int4 *d4 = reinterpret_cast<int4 *>(depth + v0);
+        const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) d4[k] = inf4;
+    } else {
+        for (uint64_t v = v0; v < n; ++v) depth[v] = kInf;
+    }
+    uint32_t bits = 0;
+    if ((root >> 5) == word) {
+        bits = 1u << (root & 31);
+        depth[root] = 0;
+        q[0] = root;
+    }
+    visited[word] = bits;
+    fbm[word] = bits;
+}
+
+// Rebuild frontier bitmap + visited bitmap from an arbitrary depth array.
+__global__ void __launch_bounds__(kBlock)
+k_prepare(const int32_t *__restrict__ depth, uint64_t n, uint64_t words, int32_t level,
+          uint32_t *fbm, uint32_t *visited, Ctr *ctr) {
+    const unsigned lane = lane_id();
+    const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+    const int64_t lvl1 = (int64_t)level + 1;
+    for (uint64_t word = warp; word < words; word += nwarps) {
+        const uint64_t v = word * 32 + lane;
+        const int32_t d = v < n ? depth[v] : kInf;
+        const unsigned fm = __ballot_sync(kFull, v < n && d == level);
+        const unsigned vm = __ballot_sync(kFull, d != kInf);
+        const bool bad = __any_sync(kFull, d != kInf && (int64_t)d > lvl1);
+        if (lane == 0) {
+            fbm[word] = fm;
+            visited[word] = vm;
+            if (fm) atomicAdd(&ctr->fcount, (unsigned long long)__popc(fm));
+            if (bad) ctr->inconsistent = 1;
+        }
+    }
+}
+
+// Σ out-degree over reached vertices (GTEPS numerator) + reached count.
+__global__ void __launch_bounds__(kBlock)
+k_reached(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_off,
+          uint64_t n, Ctr *ctr) {
+    unsigned long long e = 0, r = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * kBlock + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * kBlock) {
+        if (depth[v] != kInf) {
+            e += out_off[v + 1] - out_off[v];
+            ++r;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_down_sync(kFull, e, o);
+        r += __shfl_down_sync(kFull, r, o);
+    }
+    if (lane_id() == 0 && (e || r)) {
+        atomicAdd(&ctr->reached_edges, e);
+        atomicAdd(&ctr->reached_vertices, r);
+    }
+}
+
+// aggregate_count on the device with the three reduction shapes.
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_aggregate(const long long *__restrict__ counts, uint64_t n, unsigned long long *total) {
+    __shared__ unsigned long long part[kBlock / 32];
+    const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+    unsigned long long x = i < n ? (unsigned long long)counts[i] : 0ull;
+    if constexpr (VAR == 0) {
+        if (i < n) atomicAdd(total, x);
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(kFull, x, o);
+        if constexpr (VAR == 1) {
+            if (lane_id() == 0) atomicAdd(total, x);
+        } else {
+            if (lane_id() == 0) part[threadIdx.x >> 5] = x;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long s = 0;
+                for (int k = 0; k < kBlock / 32; ++k) s += part[k];
+                atomicAdd(total, s);
+            }
+        }
+    }
+}
+
+}  // namespace abfs

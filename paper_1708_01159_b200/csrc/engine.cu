@@ -1,0 +1,512 @@
+// engine.cu -- traversal state, level driver, bfs_full / adaptive loops and
+// the C ABI of include/abfs.h (except graph construction, see graph.cu).
+//
+// Per level: [optional prepare from caller depths] ->
+// [optional queue<->bitmap conversion] -> one strategy kernel (two for
+// push-warp: warp pass + CTA heavy pass) -> one 64-byte counter readback.
+// Host decides the next (kernel, variant) from the reference's float64
+// features and the FlatTree (adaptive.py:101-129).
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "bfs_kernels.cuh"
+
+namespace abfs {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+static uint64_t host_ns() {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+}  // namespace abfs
+
+using namespace abfs;
+
+struct abfs_traversal {
+    abfs_graph *g = nullptr;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int32_t *depth = nullptr;
+    uint32_t *visited = nullptr;
+    uint32_t *fbm[2] = {nullptr, nullptr};
+    uint32_t *q[2] = {nullptr, nullptr};
+    uint2 *units = nullptr;
+    Ctr *dctr = nullptr;
+    Ctr *hctr = nullptr;       // pinned
+    uint64_t words = 0;
+    int cur = 0;
+    bool has_q = false, has_bm = false;
+    uint64_t F = 0;            // current frontier size (host-known)
+    int64_t expect_level = -1; // level whose frontier the state holds; -1 = rebuild
+    uint64_t call = 0;
+    bool inconsistent = false;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, et0 = nullptr;
+    uint64_t last_trav_ns = 0;
+};
+
+extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
+extern "C" int abfs_version(void) { return 1; }
+
+static int level_params_ok(int64_t level, int kernel, int variant, int64_t chunk) {
+    if (kernel < 0 || kernel > 4) return fail(ABFS_EINVAL, "unknown kernel " + std::to_string(kernel));
+    if (variant < 0 || variant > 2)
+        return fail(ABFS_EINVAL, "unknown count variant " + std::to_string(variant));
+    if (kernel == ABFS_VERTEX_PUSH_WARP && chunk < 1)
+        return fail(ABFS_EINVAL, "chunk_size must be >= 1");
+    if (level < INT32_MIN || level > (int64_t)kInf - 2)
+        return fail(ABFS_EINVAL, "level out of range");
+    return ABFS_OK;
+}
+
+static inline unsigned grid_for(uint64_t items, uint64_t per_block, uint64_t cap) {
+    uint64_t b = (items + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+template <int VAR>
+static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, int64_t chunk,
+                            int out) {
+    const DevGraph &g = t->g->d;
+    cudaStream_t s = t->stream;
+    const uint32_t F = (uint32_t)t->F;
+    switch (kernel) {
+    case ABFS_EDGE_LIST:
+        k_edge<VAR, false><<<grid_for(g.m, kEdgeTile, 1ull << 31), kBlock, 0, s>>>(c, g.org, g.dst, g.m);
+        break;
+    case ABFS_REV_EDGE_LIST:
+        k_edge<VAR, true><<<grid_for(g.m, kEdgeTile, 1ull << 31), kBlock, 0, s>>>(c, g.rev_owner, g.src, g.m);
+        break;
+    case ABFS_VERTEX_PUSH:
+        k_push<VAR><<<grid_for(F, kBlock, 148 * 64), kBlock, 0, s>>>(c, t->q[t->cur], F, g.out_off, g.dst);
+        break;
+    case ABFS_VERTEX_PULL:
+        k_pull<VAR><<<grid_for(t->words, kBlock / 32, 148 * 512), kBlock, 0, s>>>(
+            c, g.in_off, g.src, t->fbm[t->cur ^ 1], g.n, t->words);
+        break;
+    default: {  // VERTEX_PUSH_WARP: nearest legal virtual-warp width <= chunk
+        const int vw = chunk >= 32 ? 32 : chunk >= 16 ? 16 : chunk >= 8 ? 8 : chunk >= 4 ? 4 : chunk >= 2 ? 2 : 1;
+        const unsigned grid = grid_for((uint64_t)F * vw, kBlock, 148 * 64);
+        unsigned int *ut = &t->dctr->units[out];
+        const uint32_t *q = t->q[t->cur];
+        switch (vw) {
+        case 32: k_push_warp<VAR, 32><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        case 16: k_push_warp<VAR, 16><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        case 8: k_push_warp<VAR, 8><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        case 4: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        case 2: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        default: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        }
+        k_heavy<VAR><<<148 * 4, kBlock, 0, s>>>(c, g.out_off, g.dst, t->units, ut);
+    }
+    }
+}
+
+// One level on the device-resident state.
+static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant, int64_t chunk,
+                      uint64_t *new_count, uint64_t *elapsed_ns, int *converted) {
+    ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
+    ABFS_CUDA(cudaSetDevice(t->device));
+    const DevGraph &g = t->g->d;
+    cudaStream_t s = t->stream;
+    int conv = 0;
+    ABFS_CUDA(cudaEventRecord(t->e0, s));
+    if (t->expect_level != level) {
+        // Frontier unknown for this level: rebuild from the depth array.
+        ABFS_CUDA(cudaMemsetAsync(&t->dctr->inconsistent, 0, sizeof(unsigned), s));
+        ABFS_CUDA(cudaMemsetAsync(&t->dctr->fcount, 0, sizeof(unsigned long long), s));
+        k_prepare<<<grid_for(t->words, kBlock / 32, 148 * 512), kBlock, 0, s>>>(
+            t->depth, g.n, t->words, (int32_t)level, t->fbm[t->cur], t->visited, t->dctr);
+        ABFS_CUDA(cudaGetLastError());
+        ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, s));
+        ABFS_CUDA(cudaStreamSynchronize(s));
+        t->F = t->hctr->fcount;
+        t->inconsistent = t->hctr->inconsistent != 0;
+        t->has_bm = true;
+        t->has_q = false;
+        t->expect_level = level;
+        conv = 1;
+    }
+    const bool need_queue = (kernel == ABFS_VERTEX_PUSH || kernel == ABFS_VERTEX_PUSH_WARP);
+    if (need_queue && !t->has_q) {
+        k_bitmap_to_queue<<<grid_for(t->words, kBlock, 1ull << 31), kBlock, 0, s>>>(
+            t->fbm[t->cur], t->words, t->q[t->cur], &t->dctr->cq);
+        t->has_q = true;
+        conv = 1;
+    } else if (!need_queue && !t->has_bm) {
+        ABFS_CUDA(cudaMemsetAsync(t->fbm[t->cur], 0, t->words * 4, s));
+        if (t->F)
+            k_queue_to_bitmap<<<grid_for(t->F, kBlock, 148 * 16), kBlock, 0, s>>>(
+                t->q[t->cur], (uint32_t)t->F, t->fbm[t->cur]);
+        t->has_bm = true;
+        conv = 1;
+    }
+    const int out = (int)(t->call % 3);
+    LevelCtx c;
+    c.depth = t->depth;
+    c.visited = t->visited;
+    c.fbm = t->fbm[t->cur];
+    c.q_next = t->q[t->cur ^ 1];
+    c.q_tail = &t->dctr->qlen[out];
+    c.count = &t->dctr->count[out];
+    c.inconsistent = &t->dctr->inconsistent;
+    c.ctr = t->dctr;
+    c.zero_slot = (int)((t->call + 1) % 3);
+    c.level = (int32_t)level;
+    c.lvl1 = (int32_t)(level + 1);
+    switch (variant) {
+    case 0: launch_strategy<0>(t, c, kernel, chunk, out); break;
+    case 1: launch_strategy<1>(t, c, kernel, chunk, out); break;
+    default: launch_strategy<2>(t, c, kernel, chunk, out); break;
+    }
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, s));
+    ABFS_CUDA(cudaEventRecord(t->e1, s));
+    ABFS_CUDA(cudaEventSynchronize(t->e1));
+    float ms = 0.f;
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->e0, t->e1));
+    t->call++;
+    const bool topdown = kernel != ABFS_VERTEX_PULL;
+    const uint64_t cnt = topdown ? (uint64_t)t->hctr->qlen[out] : (uint64_t)t->hctr->count[out];
+    t->cur ^= 1;
+    t->has_q = topdown;
+    t->has_bm = !topdown;
+    t->F = cnt;
+    // After an inconsistent level, lowered (non-counted) vertices also sit at
+    // depth level+1: the next level must rebuild its frontier from depths.
+    t->expect_level = t->inconsistent ? -1 : level + 1;
+    *new_count = cnt;
+    uint64_t ns = (uint64_t)llround((double)ms * 1e6);
+    *elapsed_ns = ns ? ns : 1;
+    if (converted) *converted = conv;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
+    if (!g || !out) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(g->device));
+    abfs_traversal *t = new abfs_traversal();
+    t->g = g;
+    t->device = g->device;
+    const uint64_t n = g->d.n, m = g->d.m;
+    t->words = (n + 31) / 32;
+    const uint64_t wpad = t->words + 4;
+    const uint64_t qcap = n + 4;
+    const uint64_t ucap = m / kHeavy + 64;
+    cudaError_t e = cudaSuccess;
+    auto A = [&](void **p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+    };
+    A((void **)&t->depth, (n + 4) * sizeof(int32_t));
+    A((void **)&t->visited, wpad * 4);
+    A((void **)&t->fbm[0], wpad * 4);
+    A((void **)&t->fbm[1], wpad * 4);
+    A((void **)&t->q[0], qcap * 4);
+    A((void **)&t->q[1], qcap * 4);
+    A((void **)&t->units, ucap * sizeof(uint2));
+    A((void **)&t->dctr, sizeof(Ctr));
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&t->hctr, sizeof(Ctr));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) t->own_stream = true;
+    if (e == cudaSuccess) e = cudaEventCreate(&t->e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&t->e1);
+    if (e == cudaSuccess) e = cudaEventCreate(&t->et0);
+    if (e == cudaSuccess) e = cudaMemset(t->dctr, 0, sizeof(Ctr));
+    if (e == cudaSuccess) e = cudaMemset(t->depth, 0xff, (n + 4) * sizeof(int32_t));
+    if (e != cudaSuccess) {
+        set_error(std::string("traversal_create: ") + cudaGetErrorString(e));
+        abfs_traversal_destroy(t);
+        return e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA;
+    }
+    *out = t;
+    return ABFS_OK;
+}
+
+extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
+    if (!t) return;
+    cudaSetDevice(t->device);
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    cudaFree(t->depth);
+    cudaFree(t->visited);
+    cudaFree(t->fbm[0]);
+    cudaFree(t->fbm[1]);
+    cudaFree(t->q[0]);
+    cudaFree(t->q[1]);
+    cudaFree(t->units);
+    cudaFree(t->dctr);
+    if (t->hctr) cudaFreeHost(t->hctr);
+    if (t->e0) cudaEventDestroy(t->e0);
+    if (t->e1) cudaEventDestroy(t->e1);
+    if (t->et0) cudaEventDestroy(t->et0);
+    if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
+    delete t;
+}
+
+extern "C" int abfs_traversal_set_stream(abfs_traversal *t, void *stream) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    if (t->own_stream) cudaStreamDestroy(t->stream);
+    if (stream) {
+        t->stream = (cudaStream_t)stream;
+        t->own_stream = false;
+    } else {
+        ABFS_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+        t->own_stream = true;
+    }
+    return ABFS_OK;
+}
+
+static int init_impl(abfs_traversal *t, int64_t root) {
+    const uint64_t n = t->g->d.n;
+    if (root < 0 || (uint64_t)root >= n)
+        return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
+                                     std::to_string(n));
+    ABFS_CUDA(cudaSetDevice(t->device));
+    t->cur = 0;
+    k_init<<<grid_for(t->words, kBlock, 1ull << 31), kBlock, 0, t->stream>>>(
+        t->depth, t->visited, t->fbm[0], t->q[0], n, t->words, (uint32_t)root);
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaMemsetAsync(&t->dctr->inconsistent, 0, sizeof(unsigned), t->stream));
+    t->has_q = true;
+    t->has_bm = true;
+    t->F = 1;
+    t->expect_level = 0;
+    t->inconsistent = false;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_init_depths(abfs_traversal *t, int64_t root) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_TRY(init_impl(t, root));
+    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_load_depths(abfs_traversal *t, const int32_t *host) {
+    if (!t || !host) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_CUDA(cudaMemcpyAsync(t->depth, host, t->g->d.n * sizeof(int32_t),
+                              cudaMemcpyHostToDevice, t->stream));
+    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    t->expect_level = -1;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
+    if (!t || !host) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_CUDA(cudaMemcpyAsync(host, t->depth, t->g->d.n * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, t->stream));
+    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_level(abfs_traversal *t, int64_t level, int kernel, int variant,
+                          int64_t chunk, uint64_t *new_count, uint64_t *elapsed_ns) {
+    if (!t || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
+    return level_impl(t, level, kernel, variant, chunk, new_count, elapsed_ns, nullptr);
+}
+
+extern "C" int abfs_run_level(abfs_traversal *t, int32_t *host, int64_t level, int kernel,
+                              int variant, int64_t chunk, uint64_t *new_count,
+                              uint64_t *elapsed_ns) {
+    if (!t || !host || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
+    ABFS_TRY(abfs_load_depths(t, host));
+    ABFS_TRY(level_impl(t, level, kernel, variant, chunk, new_count, elapsed_ns, nullptr));
+    return abfs_read_depths(t, host);
+}
+
+static int finish_traversal(abfs_traversal *t, int32_t *depths_out) {
+    float ms = 0.f;
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->e1));
+    t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
+    if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int variant,
+                             int64_t chunk, int32_t *depths_out, uint64_t *counts,
+                             uint64_t *elapsed, size_t cap, size_t *n_levels) {
+    if (!t || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(level_params_ok(0, kernel, variant, chunk));
+    ABFS_TRY(init_impl(t, root));
+    ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
+    for (int64_t level = 0;; ++level) {
+        uint64_t c = 0, el = 0;
+        ABFS_TRY(level_impl(t, level, kernel, variant, chunk, &c, &el, nullptr));
+        if ((size_t)level < cap) {
+            if (counts) counts[level] = c;
+            if (elapsed) elapsed[level] = el;
+        }
+        if (c == 0) {
+            *n_levels = (size_t)level + 1;
+            break;
+        }
+    }
+    return finish_traversal(t, depths_out);
+}
+
+extern "C" int abfs_features(const double *static24, uint64_t frontier, uint64_t discovered,
+                             double *out24) {
+    // extract_runtime_features (features.py:98-121): float64 true divisions.
+    if (!static24 || !out24) return fail(ABFS_EINVAL, "null argument");
+    const double nd = static24[0];
+    const uint64_t n = (uint64_t)nd;
+    if (n < 1) return fail(ABFS_EFEATURE, "stats must describe a non-empty graph");
+    if (discovered < frontier)
+        return fail(ABFS_EFEATURE, "need 0 <= frontier_abs <= discovered_abs, got " +
+                                       std::to_string(frontier) + " and " + std::to_string(discovered));
+    if (discovered > n)
+        return fail(ABFS_EFEATURE, "discovered_abs " + std::to_string(discovered) +
+                                       " exceeds |V|=" + std::to_string(n));
+    std::memcpy(out24, static24, 24 * sizeof(double));
+    out24[2] = (double)frontier;
+    out24[3] = (double)frontier / (double)n;
+    out24[4] = (double)discovered;
+    out24[5] = (double)discovered / (double)n;
+    return ABFS_OK;
+}
+
+static int tree_leaf(const abfs_tree *tr, const double *canonical24) {
+    // FlatTree.predict_one (tree.py:332-339): strict < goes left.
+    uint32_t node = 0;
+    while (tr->leaf_classes[node] == ABFS_NOT_A_LEAF) {
+        const double x = canonical24[tr->selection[tr->features[node]]];
+        node = (x < tr->thresholds[node]) ? tr->lefts[node] : tr->rights[node];
+    }
+    return tr->leaf_classes[node];
+}
+
+static int tree_ok(const abfs_tree *tr) {
+    if (!tr || tr->node_count == 0 || !tr->selection || !tr->features || !tr->thresholds ||
+        !tr->lefts || !tr->rights || !tr->leaf_classes)
+        return fail(ABFS_EINVAL, "invalid tree");
+    for (uint32_t i = 0; i < tr->n_selection; ++i)
+        if (tr->selection[i] >= ABFS_N_FEATURES) return fail(ABFS_EINVAL, "bad selection index");
+    for (uint32_t k = 0; k < tr->node_count; ++k) {
+        const uint8_t c = tr->leaf_classes[k];
+        if (c == ABFS_NOT_A_LEAF) {
+            if (tr->features[k] >= tr->n_selection || tr->lefts[k] >= tr->node_count ||
+                tr->rights[k] >= tr->node_count || tr->lefts[k] <= k || tr->rights[k] <= k)
+                return fail(ABFS_EINVAL, "malformed tree node " + std::to_string(k));
+        } else if (c >= 15 && c != ABFS_LEAF_UNKNOWN) {
+            return fail(ABFS_EINVAL, "bad leaf class " + std::to_string(c));
+        }
+    }
+    return ABFS_OK;
+}
+
+extern "C" int abfs_tree_predict(const abfs_tree *tr, const double *projected, int *leaf) {
+    if (!projected || !leaf) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(tree_ok(tr));
+    uint32_t node = 0;
+    while (tr->leaf_classes[node] == ABFS_NOT_A_LEAF) {
+        const double x = projected[tr->features[node]];
+        node = (x < tr->thresholds[node]) ? tr->lefts[node] : tr->rights[node];
+    }
+    *leaf = tr->leaf_classes[node];
+    return ABFS_OK;
+}
+
+extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree *tr,
+                                 const double *static24, int64_t chunk, int32_t *depths_out,
+                                 abfs_level_record *recs, size_t cap, size_t *n_levels) {
+    if (!t || !static24 || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(tree_ok(tr));
+    ABFS_TRY(init_impl(t, root));
+    ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
+    uint64_t frontier = 1, discovered = 1;
+    int pk = ABFS_EDGE_LIST, pv = ABFS_DIRECT_ATOMIC;  // DEFAULT_KERNEL adaptive.py:36-38
+    double vec[24];
+    for (int64_t level = 0;; ++level) {
+        const uint64_t t0 = host_ns();
+        ABFS_TRY(abfs_features(static24, frontier, discovered, vec));
+        const int cls = tree_leaf(tr, vec);
+        const uint64_t pred = host_ns() - t0;
+        const int fallback = cls == ABFS_LEAF_UNKNOWN;
+        if (!fallback) {
+            pk = cls / 3;
+            pv = cls % 3;
+        }
+        uint64_t c = 0, el = 0;
+        int conv = 0;
+        ABFS_TRY(level_impl(t, level, pk, pv, chunk, &c, &el, &conv));
+        if (recs && (size_t)level < cap) {
+            abfs_level_record &r = recs[level];
+            r.level = level;
+            r.kernel = pk;
+            r.variant = pv;
+            r.fallback = fallback;
+            r.converted = conv;
+            r.frontier_size = frontier;
+            r.new_count = c;
+            r.elapsed_ns = el;
+            r.prediction_ns = pred ? pred : 1;
+        }
+        if (c == 0) {
+            *n_levels = (size_t)level + 1;
+            break;
+        }
+        frontier = c;
+        discovered += c;
+    }
+    return finish_traversal(t, depths_out);
+}
+
+extern "C" int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns) {
+    if (!t || !ns) return fail(ABFS_EINVAL, "null argument");
+    *ns = t->last_trav_ns;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices) {
+    if (!t || !edges || !vertices) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_CUDA(cudaMemsetAsync(&t->dctr->reached_edges, 0, 16, t->stream));
+    k_reached<<<148 * 8, kBlock, 0, t->stream>>>(t->depth, t->g->d.out_off, t->g->d.n, t->dctr);
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, t->stream));
+    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    *edges = t->hctr->reached_edges;
+    *vertices = t->hctr->reached_vertices;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_aggregate_count(int device, const int64_t *host_counts, size_t n,
+                                    int variant, int64_t *total) {
+    if (!total || (n && !host_counts)) return fail(ABFS_EINVAL, "null argument");
+    if (variant < 0 || variant > 2)
+        return fail(ABFS_EINVAL, "unknown count variant " + std::to_string(variant));
+    ABFS_CUDA(cudaSetDevice(device));
+    long long *d = nullptr;
+    unsigned long long *dt = nullptr;
+    ABFS_CUDA(cudaMalloc(&d, (n ? n : 1) * sizeof(long long)));
+    cudaError_t e = cudaMalloc(&dt, sizeof(unsigned long long));
+    if (e == cudaSuccess && n) e = cudaMemcpy(d, host_counts, n * sizeof(long long), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dt, 0, sizeof(unsigned long long));
+    if (e == cudaSuccess && n) {
+        const unsigned grid = grid_for(n, kBlock, 1ull << 31);
+        if (variant == 0) k_aggregate<0><<<grid, kBlock>>>(d, n, dt);
+        else if (variant == 1) k_aggregate<1><<<grid, kBlock>>>(d, n, dt);
+        else k_aggregate<2><<<grid, kBlock>>>(d, n, dt);
+        e = cudaGetLastError();
+    }
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&h, dt, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(dt);
+    if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("aggregate_count: ") + cudaGetErrorString(e));
+    *total = (int64_t)h;
+    return ABFS_OK;
+}

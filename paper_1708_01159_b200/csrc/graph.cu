@@ -1,0 +1,494 @@
+// graph.cu -- device-resident combined representation: upload, device
+// build_combined (graph.py:93-134) and bit-exact device generators
+// (generate_graph, graph.py:211-252) for the K24/K26/ER/mesh configs.
+//
+// build_combined on the device: pack each edge as a 64-bit key
+// (src << 32 | dst) and radix-sort it (CUB) -> forward CSR order
+// (lexsort by (src, dst)); pack (dst << 32 | src) and sort -> reverse order
+// (lexsort by (dst, src)) whose high words are rev_owner for free.  Offsets
+// come from a boundary pass over the sorted high words.
+//
+// Generators reproduce numpy's PCG64 stream (state = state*M + inc, XSL-RR
+// output) with jump-ahead, so a thread can start anywhere in the stream:
+//   rmat-like:  draw index bit*m + i for edge i at bit level `bit`,
+//               random() = (x >> 11) * 2^-53 compared against the cumulative
+//               quadrant probabilities (compared exactly as integers
+//               k >= ceil(t * 2^53));
+//   uniform:    u32 half-words low-then-high, src = u32[0:m],
+//               dst = u32[m:2m], value = u32 * n >> 32 (n a power of two:
+//               Lemire's rejection never fires).
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+using namespace abfs;
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+__host__ __device__ inline u128 pcg_mult() {
+    return ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
+}
+
+__device__ __forceinline__ uint64_t pcg_out(u128 s) {
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const uint64_t x = hi ^ lo;
+    const unsigned r = (unsigned)(hi >> 58);
+    return (x >> r) | (x << ((64 - r) & 63));
+}
+
+// Affine map of `delta` LCG steps: s -> A*s + C.
+__host__ __device__ inline void pcg_jump(u128 inc, u128 delta, u128 &A, u128 &C) {
+    u128 am = 1, ap = 0, cm = pcg_mult(), cp = inc;
+    while (delta) {
+        if (delta & 1) {
+            am *= cm;
+            ap = ap * cm + cp;
+        }
+        cp = (cm + 1) * cp;
+        cm *= cm;
+        delta >>= 1;
+    }
+    A = am;
+    C = ap;
+}
+
+struct RmatParams {
+    u128 s0, inc;
+    uint64_t m;
+    uint64_t t1, t2, t3;   // integer thresholds ceil(a*2^53), ceil((a+b)*2^53), ...
+    uint32_t scale;
+    u128 bitA[64], bitC[64];  // jump from stream position i to bit*m + i
+    int symmetrize;
+};
+
+constexpr int kGenChunk = 16;
+
+__global__ void k_gen_rmat(const RmatParams *__restrict__ P, uint64_t *keys_fwd) {
+    const RmatParams &p = *P;
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kGenChunk;
+    if (i0 >= p.m) return;
+    const int cnt = (int)min((uint64_t)kGenChunk, p.m - i0);
+    u128 A, C;
+    pcg_jump(p.inc, (u128)i0, A, C);
+    const u128 base = A * p.s0 + C;  // state before draw i0 at bit 0
+    uint32_t src[kGenChunk], dst[kGenChunk];
+#pragma unroll
+    for (int k = 0; k < kGenChunk; ++k) src[k] = dst[k] = 0;
+    const u128 M = pcg_mult();
+    for (uint32_t bit = 0; bit < p.scale; ++bit) {
+        u128 s = p.bitA[bit] * base + p.bitC[bit];
+#pragma unroll
+        for (int k = 0; k < kGenChunk; ++k) {
+            if (k < cnt) {
+                s = s * M + p.inc;
+                const uint64_t r = pcg_out(s) >> 11;
+                const uint32_t sb = r >= p.t2;
+                const uint32_t db = (r >= p.t1 && r < p.t2) || r >= p.t3;
+                src[k] = (src[k] << 1) | sb;
+                dst[k] = (dst[k] << 1) | db;
+            }
+        }
+    }
+    for (int k = 0; k < cnt; ++k) {
+        keys_fwd[i0 + k] = ((uint64_t)src[k] << 32) | dst[k];
+        if (p.symmetrize) keys_fwd[p.m + i0 + k] = ((uint64_t)dst[k] << 32) | src[k];
+    }
+}
+
+struct UniParams {
+    u128 s0, inc;
+    uint64_t n_log2, m;
+};
+
+// u64 draw k yields u32 stream positions 2k (low) and 2k+1 (high).
+__global__ void k_gen_uniform(UniParams p, uint64_t *keys) {
+    const uint64_t k0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kGenChunk;
+    const uint64_t draws = p.m;  // 2m half-words
+    if (k0 >= draws) return;
+    u128 A, C;
+    pcg_jump(p.inc, (u128)k0, A, C);
+    u128 s = A * p.s0 + C;
+    const u128 M = pcg_mult();
+    const uint64_t cnt = min((uint64_t)kGenChunk, draws - k0);
+    uint32_t *key32 = reinterpret_cast<uint32_t *>(keys);  // little-endian: [2i]=lo(dst), [2i+1]=hi(src)
+    for (uint64_t k = 0; k < cnt; ++k) {
+        s = s * M + p.inc;
+        const uint64_t o = pcg_out(s);
+        const uint64_t j0 = 2 * (k0 + k);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint64_t j = j0 + h;
+            const uint64_t u = h ? (o >> 32) : (o & 0xffffffffull);
+            const uint32_t val = (uint32_t)((u << p.n_log2) >> 32);
+            if (j < p.m) key32[2 * j + 1] = val;           // src -> high word
+            else key32[2 * (j - p.m)] = val;               // dst -> low word
+        }
+    }
+}
+
+__global__ void k_gen_mesh(uint32_t rows, uint32_t cols, uint64_t *keys, unsigned long long *cursor) {
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t n = (uint64_t)rows * cols;
+    if (v >= n) return;
+    const uint32_t r = (uint32_t)(v / cols), c = (uint32_t)(v % cols);
+    uint64_t nb[4];
+    int k = 0;
+    if (r > 0) nb[k++] = v - cols;
+    if (c > 0) nb[k++] = v - 1;
+    if (c + 1 < cols) nb[k++] = v + 1;
+    if (r + 1 < rows) nb[k++] = v + cols;
+    if (!k) return;
+    const unsigned long long p = atomicAdd(cursor, (unsigned long long)k);
+    for (int i = 0; i < k; ++i) keys[p + i] = (v << 32) | nb[i];
+}
+
+__global__ void k_pack_pairs(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                             uint64_t m, uint64_t *keys) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = ((uint64_t)a[i] << 32) | b[i];
+}
+
+// Split sorted keys into (hi, lo) arrays and write CSR offsets: off[v] is the
+// first index whose hi >= v (boundary pass, O(m + n)).
+__global__ void k_split_offsets(const uint64_t *__restrict__ keys, uint64_t m, uint64_t n,
+                                uint32_t *hi_out, uint32_t *lo_out, uint32_t *off) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t cur = i < m ? (keys[i] >> 32) : n;
+        const int64_t prev = i > 0 ? (int64_t)(keys[i - 1] >> 32) : -1;
+        if (i < m) {
+            if (hi_out) hi_out[i] = (uint32_t)(keys[i] >> 32);
+            lo_out[i] = (uint32_t)keys[i];
+        }
+        for (int64_t v = prev + 1; v <= (int64_t)cur && v <= (int64_t)n; ++v) off[v] = (uint32_t)i;
+    }
+}
+
+// rev_owner from in_offsets (upload path): binary search per slot.
+__global__ void k_rev_owner(const uint32_t *__restrict__ in_off, uint64_t n, uint64_t m,
+                            uint32_t *owner) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = n;  // last v with in_off[v] <= e
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (in_off[mid] <= e) lo = mid;
+            else hi = mid;
+        }
+        owner[e] = (uint32_t)lo;
+    }
+}
+
+inline unsigned grid_cap(uint64_t items, unsigned block, uint64_t cap = 148ull * 64) {
+    uint64_t b = (items + block - 1) / block;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+int bits_for(uint64_t n) {
+    int b = 0;
+    while (b < 32 && (1ull << b) < n) ++b;
+    return b;
+}
+
+// Sort `keys` (m entries, significant bits: 32 + vbits) with CUB; result in
+// *keys_io (may swap with alt).
+int sort_keys(uint64_t *&keys, uint64_t *&alt, uint64_t m, int vbits, cudaStream_t s) {
+    if (m == 0) return ABFS_OK;
+    cub::DoubleBuffer<uint64_t> db(keys, alt);
+    size_t tmp = 0;
+    ABFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)m, 0, 32 + vbits, s));
+    void *dtmp = nullptr;
+    ABFS_CUDA(cudaMallocAsync(&dtmp, tmp, s));
+    // Low word holds the minor key; sort all of it plus the used high bits.
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(dtmp, tmp, db, (int64_t)m, 0, 32 + vbits, s);
+    cudaFreeAsync(dtmp, s);
+    if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    if (db.Current() != keys) std::swap(keys, alt);
+    return ABFS_OK;
+}
+
+// keys: forward-packed (src<<32|dst), m entries, device; consumed.
+int build_from_keys(abfs_graph *g, uint64_t *keys, uint64_t *alt, cudaStream_t s) {
+    DevGraph &d = g->d;
+    const uint64_t n = d.n, m = d.m;
+    const int vb = bits_for(n);
+    ABFS_TRY(sort_keys(keys, alt, m, vb, s));
+    k_split_offsets<<<grid_cap(m + 1, 256), 256, 0, s>>>(keys, m, n, d.org, d.dst, d.out_off);
+    ABFS_CUDA(cudaGetLastError());
+    // reverse: (dst << 32 | src) from the forward arrays
+    k_pack_pairs<<<grid_cap(m, 256), 256, 0, s>>>(d.dst, d.org, m, keys);
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_TRY(sort_keys(keys, alt, m, vb, s));
+    k_split_offsets<<<grid_cap(m + 1, 256), 256, 0, s>>>(keys, m, n, d.rev_owner, d.src, d.in_off);
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    return ABFS_OK;
+}
+
+struct KeyBufs {
+    uint64_t *a = nullptr, *b = nullptr;
+    ~KeyBufs() {
+        cudaFree(a);
+        cudaFree(b);
+    }
+};
+
+int new_graph(int device, uint64_t n, uint64_t m, abfs_graph **out) {
+    if (!out) return fail(ABFS_EINVAL, "null output");
+    if (n >= (1ull << 32)) return fail(ABFS_EINVAL, "vertex_count must be < 2^32");
+    if (m >= (1ull << 32)) return fail(ABFS_EINVAL, "edge_count must be < 2^32 (u32 offsets)");
+    ABFS_CUDA(cudaSetDevice(device));
+    abfs_graph *g = new abfs_graph();
+    g->device = device;
+    int rc = graph_alloc(g, n, m);
+    if (rc) {
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return ABFS_OK;
+}
+
+int finish_build(int rc, abfs_graph *g, abfs_graph **out) {
+    if (rc != ABFS_OK) {
+        abfs_graph_destroy(g);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+}  // namespace
+
+namespace abfs {
+
+int graph_alloc(abfs_graph *g, uint64_t n, uint64_t m) {
+    DevGraph &d = g->d;
+    d.n = n;
+    d.m = m;
+    const size_t mb = (m ? m : 1) * 4 + 16;
+    cudaError_t e = cudaSuccess;
+    auto A = [&](uint32_t **p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc((void **)p, bytes);
+    };
+    A(&d.out_off, (n + 1) * 4 + 16);
+    A(&d.in_off, (n + 1) * 4 + 16);
+    A(&d.dst, mb);
+    A(&d.org, mb);
+    A(&d.src, mb);
+    A(&d.rev_owner, mb);
+    if (e != cudaSuccess) {
+        graph_free(g);
+        return fail(e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA,
+                    std::string("graph alloc: ") + cudaGetErrorString(e));
+    }
+    return ABFS_OK;
+}
+
+void graph_free(abfs_graph *g) {
+    DevGraph &d = g->d;
+    cudaFree(d.out_off);
+    cudaFree(d.in_off);
+    cudaFree(d.dst);
+    cudaFree(d.org);
+    cudaFree(d.src);
+    cudaFree(d.rev_owner);
+    d = DevGraph();
+}
+
+}  // namespace abfs
+
+extern "C" void abfs_graph_destroy(abfs_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    graph_free(g);
+    delete g;
+}
+
+extern "C" int abfs_graph_info(const abfs_graph *g, uint64_t *n, uint64_t *m, int *device) {
+    if (!g) return fail(ABFS_EINVAL, "null graph");
+    if (n) *n = g->d.n;
+    if (m) *m = g->d.m;
+    if (device) *device = g->device;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_graph_upload(int device, uint64_t n, uint64_t m, const uint32_t *out_offsets,
+                                 const uint32_t *destinations, const uint32_t *origins,
+                                 const uint32_t *in_offsets, const uint32_t *sources,
+                                 abfs_graph **out) {
+    if (!out_offsets || !in_offsets || (m && (!destinations || !origins || !sources)))
+        return fail(ABFS_EINVAL, "null array");
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, m, &g));
+    DevGraph &d = g->d;
+    int rc = ABFS_OK;
+    auto up = [&](uint32_t *dptr, const uint32_t *h, uint64_t cnt) {
+        if (rc == ABFS_OK && cnt) {
+            cudaError_t e = cudaMemcpy(dptr, h, cnt * 4, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
+        }
+    };
+    up(d.out_off, out_offsets, n + 1);
+    up(d.in_off, in_offsets, n + 1);
+    up(d.dst, destinations, m);
+    up(d.org, origins, m);
+    up(d.src, sources, m);
+    if (rc == ABFS_OK && m) {
+        k_rev_owner<<<grid_cap(m, 256), 256>>>(d.in_off, n, m, d.rev_owner);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("rev_owner: ") + cudaGetErrorString(e));
+    }
+    *out = g;
+    return finish_build(rc, g, out);
+}
+
+extern "C" int abfs_graph_download(const abfs_graph *g, uint32_t *out_offsets,
+                                   uint32_t *destinations, uint32_t *origins,
+                                   uint32_t *in_offsets, uint32_t *sources, uint32_t *rev_owner) {
+    if (!g) return fail(ABFS_EINVAL, "null graph");
+    ABFS_CUDA(cudaSetDevice(g->device));
+    const DevGraph &d = g->d;
+    auto down = [&](uint32_t *h, const uint32_t *dp, uint64_t cnt) -> cudaError_t {
+        if (!h || !cnt) return cudaSuccess;
+        return cudaMemcpy(h, dp, cnt * 4, cudaMemcpyDeviceToHost);
+    };
+    ABFS_CUDA(down(out_offsets, d.out_off, d.n + 1));
+    ABFS_CUDA(down(in_offsets, d.in_off, d.n + 1));
+    ABFS_CUDA(down(destinations, d.dst, d.m));
+    ABFS_CUDA(down(origins, d.org, d.m));
+    ABFS_CUDA(down(sources, d.src, d.m));
+    ABFS_CUDA(down(rev_owner, d.rev_owner, d.m));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_graph_build(int device, uint64_t n, uint64_t m, const uint32_t *src,
+                                const uint32_t *dst, abfs_graph **out) {
+    if (m && (!src || !dst)) return fail(ABFS_EINVAL, "null array");
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, m, &g));
+    KeyBufs kb;
+    int rc = ABFS_OK;
+    cudaError_t e = cudaMalloc(&kb.a, (m ? m : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kb.b, (m ? m : 1) * 8);
+    // stage pairs through the (not yet filled) dst/org arrays
+    if (e == cudaSuccess && m) e = cudaMemcpy(g->d.org, src, m * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(g->d.dst, dst, m * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("build: ") + cudaGetErrorString(e));
+    if (rc == ABFS_OK && m) {
+        k_pack_pairs<<<grid_cap(m, 256), 256>>>(g->d.org, g->d.dst, m, kb.a);
+        if ((e = cudaGetLastError()) != cudaSuccess) rc = fail(ABFS_ECUDA, cudaGetErrorString(e));
+    }
+    if (rc == ABFS_OK) rc = build_from_keys(g, kb.a, kb.b, 0);
+    *out = g;
+    return finish_build(rc, g, out);
+}
+
+static u128 words_to_u128(const uint64_t w[2]) { return ((u128)w[0] << 64) | (u128)w[1]; }
+
+static uint64_t thr53(double t) {
+    // r >= t  <=>  k >= ceil(t * 2^53) for r = k * 2^-53, 0 <= k < 2^53
+    if (t <= 0.0) return 0;
+    const double x = std::ceil(t * 9007199254740992.0);
+    if (x >= 18446744073709551615.0) return ~0ull;
+    return (uint64_t)x;
+}
+
+extern "C" int abfs_graph_generate_rmat(int device, uint32_t scale, uint64_t edges, double a,
+                                        double b, double c, const uint64_t pcg_state[2],
+                                        const uint64_t pcg_inc[2], int symmetrize,
+                                        abfs_graph **out) {
+    if (!pcg_state || !pcg_inc) return fail(ABFS_EINVAL, "null pcg state");
+    if (scale < 1 || scale > 31) return fail(ABFS_EINVAL, "scale must be in [1, 31]");
+    if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0 + 1e-9)
+        return fail(ABFS_EINVAL, "rmat probabilities must be non-negative and sum to <= 1");
+    const uint64_t n = 1ull << scale;
+    const uint64_t m = symmetrize ? 2 * edges : edges;
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, m, &g));
+    RmatParams hp;
+    hp.s0 = words_to_u128(pcg_state);
+    hp.inc = words_to_u128(pcg_inc);
+    hp.m = edges;
+    hp.scale = scale;
+    hp.symmetrize = symmetrize ? 1 : 0;
+    // Same float64 operations as graph.py:247-248: a+b and (a+b)+c.
+    hp.t1 = thr53(a);
+    hp.t2 = thr53(a + b);
+    hp.t3 = thr53(a + b + c);
+    for (uint32_t bit = 0; bit < scale; ++bit) pcg_jump(hp.inc, (u128)bit * edges, hp.bitA[bit], hp.bitC[bit]);
+    KeyBufs kb;
+    RmatParams *dp = nullptr;
+    int rc = ABFS_OK;
+    cudaError_t e = cudaMalloc(&kb.a, (m ? m : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kb.b, (m ? m : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&dp, sizeof(RmatParams));
+    if (e == cudaSuccess) e = cudaMemcpy(dp, &hp, sizeof(RmatParams), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && edges) {
+        const uint64_t threads = (edges + kGenChunk - 1) / kGenChunk;
+        k_gen_rmat<<<(unsigned)((threads + 255) / 256), 256>>>(dp, kb.a);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("generate_rmat: ") + cudaGetErrorString(e));
+    if (rc == ABFS_OK) rc = build_from_keys(g, kb.a, kb.b, 0);
+    cudaFree(dp);
+    *out = g;
+    return finish_build(rc, g, out);
+}
+
+extern "C" int abfs_graph_generate_uniform(int device, uint64_t n, uint64_t edges,
+                                           const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                                           abfs_graph **out) {
+    if (!pcg_state || !pcg_inc) return fail(ABFS_EINVAL, "null pcg state");
+    if (n == 0 || (n & (n - 1)) || n > (1ull << 31))
+        return fail(ABFS_EINVAL, "device uniform-random needs a power-of-two n <= 2^31");
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, edges, &g));
+    UniParams p;
+    p.s0 = words_to_u128(pcg_state);
+    p.inc = words_to_u128(pcg_inc);
+    p.n_log2 = (uint64_t)bits_for(n);
+    p.m = edges;
+    KeyBufs kb;
+    int rc = ABFS_OK;
+    cudaError_t e = cudaMalloc(&kb.a, (edges ? edges : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kb.b, (edges ? edges : 1) * 8);
+    if (e == cudaSuccess && edges) {
+        const uint64_t threads = (edges + kGenChunk - 1) / kGenChunk;
+        k_gen_uniform<<<(unsigned)((threads + 255) / 256), 256>>>(p, kb.a);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("generate_uniform: ") + cudaGetErrorString(e));
+    if (rc == ABFS_OK) rc = build_from_keys(g, kb.a, kb.b, 0);
+    *out = g;
+    return finish_build(rc, g, out);
+}
+
+extern "C" int abfs_graph_generate_mesh(int device, uint32_t rows, uint32_t cols, abfs_graph **out) {
+    if (rows < 1 || cols < 1) return fail(ABFS_EINVAL, "mesh needs rows, cols >= 1");
+    const uint64_t n = (uint64_t)rows * cols;
+    const uint64_t m = 2 * ((uint64_t)rows * (cols - 1) + (uint64_t)(rows - 1) * cols);
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, m, &g));
+    KeyBufs kb;
+    unsigned long long *cur = nullptr;
+    int rc = ABFS_OK;
+    cudaError_t e = cudaMalloc(&kb.a, (m ? m : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kb.b, (m ? m : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cur, 8);
+    if (e == cudaSuccess) e = cudaMemset(cur, 0, 8);
+    if (e == cudaSuccess) {
+        k_gen_mesh<<<(unsigned)((n + 255) / 256), 256>>>(rows, cols, kb.a, cur);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("generate_mesh: ") + cudaGetErrorString(e));
+    if (rc == ABFS_OK) rc = build_from_keys(g, kb.a, kb.b, 0);
+    cudaFree(cur);
+    *out = g;
+    return finish_build(rc, g, out);
+}

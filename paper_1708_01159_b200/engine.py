@@ -1,0 +1,228 @@
+"""Device-resident graph and traversal handles over libabfs.so.
+
+`DeviceGraph` owns the combined representation in HBM (out-CSR, origins,
+in-CSR, rev_owner); `Traversal` owns one BFS state (depths, visited bitmap,
+frontier queue/bitmap pair, counters) and a CUDA stream.  These are the
+objects the reference-named functions in kernels.py / adaptive.py drive.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+
+
+class DeviceGraph:
+    """A Graph (graph.py:27-69) resident on one GPU."""
+
+    def __init__(self, handle: ctypes.c_void_p, host=None):
+        self._h = handle
+        n, m, dev = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int()
+        L.check(L.lib().abfs_graph_info(handle, ctypes.byref(n), ctypes.byref(m),
+                                        ctypes.byref(dev)), "graph_info")
+        self.vertex_count = n.value
+        self.edge_count = m.value
+        self.device = dev.value
+        self._host = host
+        self._scratch = None
+
+    # -- constructors -------------------------------------------------------
+    @classmethod
+    def upload(cls, graph, device: int = 0) -> "DeviceGraph":
+        a = [np.ascontiguousarray(getattr(graph, k), dtype=np.uint32) for k in
+             ("out_offsets", "destinations", "origins", "in_offsets", "sources")]
+        h = ctypes.c_void_p()
+        L.check(L.lib().abfs_graph_upload(device, graph.vertex_count, graph.edge_count,
+                                          *[L.ptr(x, L.u32p) for x in a], ctypes.byref(h)),
+                "graph_upload")
+        return cls(h, host=graph)
+
+    @classmethod
+    def build(cls, vertex_count: int, src, dst, device: int = 0) -> "DeviceGraph":
+        """Device build_combined (graph.py:93-134) from range-checked pairs."""
+        s = np.ascontiguousarray(src, dtype=np.uint32)
+        d = np.ascontiguousarray(dst, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        L.check(L.lib().abfs_graph_build(device, vertex_count, s.size, L.ptr(s, L.u32p),
+                                         L.ptr(d, L.u32p), ctypes.byref(h)), "graph_build")
+        return cls(h)
+
+    @classmethod
+    def rmat(cls, scale: int, edges: int, seed: int, a=0.57, b=0.19, c=0.19,
+             symmetrize: bool = False, device: int = 0) -> "DeviceGraph":
+        """generate_graph("rmat-like", ...) (graph.py:232-252) on the device,
+        optionally symmetrised by appending reversed pairs."""
+        st, inc = pcg_words(seed)
+        h = ctypes.c_void_p()
+        L.check(L.lib().abfs_graph_generate_rmat(device, scale, edges, a, b, c,
+                                                 L.ptr(st, L.u64p), L.ptr(inc, L.u64p),
+                                                 int(symmetrize), ctypes.byref(h)),
+                "generate_rmat")
+        return cls(h)
+
+    @classmethod
+    def uniform(cls, n: int, edges: int, seed: int, device: int = 0) -> "DeviceGraph":
+        """generate_graph("uniform-random", ...) (graph.py:226-231), n = 2^k."""
+        st, inc = pcg_words(seed)
+        h = ctypes.c_void_p()
+        L.check(L.lib().abfs_graph_generate_uniform(device, n, edges, L.ptr(st, L.u64p),
+                                                    L.ptr(inc, L.u64p), ctypes.byref(h)),
+                "generate_uniform")
+        return cls(h)
+
+    @classmethod
+    def mesh(cls, rows: int, cols: int, device: int = 0) -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        L.check(L.lib().abfs_graph_generate_mesh(device, rows, cols, ctypes.byref(h)),
+                "generate_mesh")
+        return cls(h)
+
+    # -- host views -----------------------------------------------------------
+    def download(self, rev_owner: bool = False) -> dict:
+        n, m = self.vertex_count, self.edge_count
+        out = {"out_offsets": np.empty(n + 1, np.uint32), "destinations": np.empty(m, np.uint32),
+               "origins": np.empty(m, np.uint32), "in_offsets": np.empty(n + 1, np.uint32),
+               "sources": np.empty(m, np.uint32)}
+        ro = np.empty(m, np.uint32) if rev_owner else None
+        L.check(L.lib().abfs_graph_download(
+            self._h, L.ptr(out["out_offsets"], L.u32p), L.ptr(out["destinations"], L.u32p),
+            L.ptr(out["origins"], L.u32p), L.ptr(out["in_offsets"], L.u32p),
+            L.ptr(out["sources"], L.u32p), L.ptr(ro, L.u32p) if ro is not None else None),
+            "graph_download")
+        if ro is not None:
+            out["rev_owner"] = ro
+        return out
+
+    def offsets(self):
+        """(out_offsets, in_offsets) on the host -- enough for compute_stats."""
+        n = self.vertex_count
+        oo, io = np.empty(n + 1, np.uint32), np.empty(n + 1, np.uint32)
+        L.check(L.lib().abfs_graph_download(self._h, L.ptr(oo, L.u32p), None, None,
+                                            L.ptr(io, L.u32p), None, None), "graph_download")
+        return oo, io
+
+    def to_graph(self):
+        from .graph import Graph
+        a = self.download()
+        return Graph(self.vertex_count, self.edge_count, a["out_offsets"], a["destinations"],
+                     a["origins"], a["in_offsets"], a["sources"])
+
+    def scratch(self) -> "Traversal":
+        """Cached traversal used by the stateless reference-style calls."""
+        if self._scratch is None:
+            self._scratch = Traversal(self)
+        return self._scratch
+
+    def close(self):
+        if self._scratch is not None:
+            self._scratch.close()
+            self._scratch = None
+        if self._h:
+            L.lib().abfs_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Traversal:
+    """Device BFS state over a DeviceGraph (depths + frontier + counters)."""
+
+    def __init__(self, dgraph: DeviceGraph):
+        self.graph = dgraph
+        self._h = ctypes.c_void_p()
+        L.check(L.lib().abfs_traversal_create(dgraph._h, ctypes.byref(self._h)),
+                "traversal_create")
+
+    def set_stream(self, cuda_stream_ptr: int | None):
+        L.check(L.lib().abfs_traversal_set_stream(self._h, ctypes.c_void_p(cuda_stream_ptr or 0)),
+                "set_stream")
+
+    def init(self, root: int):
+        L.check(L.lib().abfs_init_depths(self._h, int(root)), "init_depths")
+
+    def load(self, depths: np.ndarray):
+        d = np.ascontiguousarray(depths, dtype=np.int32)
+        L.check(L.lib().abfs_load_depths(self._h, L.ptr(d, L.i32p)), "load_depths")
+
+    def read(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.graph.vertex_count, dtype=np.int32)
+        L.check(L.lib().abfs_read_depths(self._h, L.ptr(out, L.i32p)), "read_depths")
+        return out
+
+    def level(self, level: int, kernel: int, variant: int, chunk_size: int = 32):
+        c, el = ctypes.c_uint64(), ctypes.c_uint64()
+        L.check(L.lib().abfs_level(self._h, int(level), int(kernel), int(variant),
+                                   int(chunk_size), ctypes.byref(c), ctypes.byref(el)),
+                "level")
+        return c.value, el.value
+
+    def run_level_host(self, depths: np.ndarray, level: int, kernel: int, variant: int,
+                       chunk_size: int = 32):
+        assert depths.dtype == np.int32 and depths.flags.c_contiguous and depths.flags.writeable
+        c, el = ctypes.c_uint64(), ctypes.c_uint64()
+        L.check(L.lib().abfs_run_level(self._h, L.ptr(depths, L.i32p), int(level), int(kernel),
+                                       int(variant), int(chunk_size), ctypes.byref(c),
+                                       ctypes.byref(el)), "run_level")
+        return c.value, el.value
+
+    def bfs_full(self, root: int, kernel: int, variant: int, chunk_size: int = 32,
+                 depths_out: np.ndarray | None = None, cap: int = 1 << 20):
+        counts = np.zeros(cap, np.uint64)
+        el = np.zeros(cap, np.uint64)
+        nl = ctypes.c_size_t()
+        L.check(L.lib().abfs_bfs_full(self._h, int(root), int(kernel), int(variant),
+                                      int(chunk_size),
+                                      L.ptr(depths_out, L.i32p) if depths_out is not None else None,
+                                      L.ptr(counts, L.u64p), L.ptr(el, L.u64p), cap,
+                                      ctypes.byref(nl)), "bfs_full")
+        k = min(nl.value, cap)
+        return counts[:k], el[:k]
+
+    def adaptive(self, root: int, tree: L.AbfsTree, static24: np.ndarray, chunk_size: int = 32,
+                 depths_out: np.ndarray | None = None, cap: int = 1 << 16):
+        recs = (L.AbfsLevelRecord * cap)()
+        nl = ctypes.c_size_t()
+        st = np.ascontiguousarray(static24, dtype=np.float64)
+        L.check(L.lib().abfs_adaptive_bfs(
+            self._h, int(root), ctypes.byref(tree), L.ptr(st, L.f64p), int(chunk_size),
+            L.ptr(depths_out, L.i32p) if depths_out is not None else None, recs, cap,
+            ctypes.byref(nl)), "adaptive_bfs")
+        return recs[:min(nl.value, cap)]
+
+    def last_ns(self) -> int:
+        v = ctypes.c_uint64()
+        L.check(L.lib().abfs_last_traversal_ns(self._h, ctypes.byref(v)), "last_ns")
+        return v.value
+
+    def reached(self):
+        e, v = ctypes.c_uint64(), ctypes.c_uint64()
+        L.check(L.lib().abfs_reached_edges(self._h, ctypes.byref(e), ctypes.byref(v)), "reached")
+        return e.value, v.value
+
+    def close(self):
+        if self._h:
+            L.lib().abfs_traversal_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pcg_words(seed: int):
+    """numpy default_rng(seed)'s PCG64 (state, inc) as (hi, lo) u64 words."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    s, i = st["state"], st["inc"]
+    return (np.array([s >> 64, s & m64], dtype=np.uint64),
+            np.array([i >> 64, i & m64], dtype=np.uint64))

@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA engine (through the reference-named API, i.e. the
+C ABI) against the reference's golden vectors and the CPU oracle.
+
+Bit-exact bar: depth arrays, per-level new counts, and the
+adaptive trace (kernel, variant, fallback, frontier) given the same tree.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import golden_util as G
+import oracle
+import paper_1708_01159_b200 as P
+from paper_1708_01159_b200.graph import stats_from_offsets
+
+pytestmark = pytest.mark.gpu
+
+_GRAPHS = {}
+
+
+def graph(name):
+    if name not in _GRAPHS:
+        n, m, a = G.graph_arrays(name)
+        _GRAPHS[name] = P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS])
+    return _GRAPHS[name]
+
+
+NAMES = G.graph_names()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_all_15_pairs_match_reference(name):
+    g = graph(name)
+    for r in G.roots(name):
+        want = G.depth(name, r)
+        cnt = G.counts(name, r).tolist()
+        for k, v in P.ALL_PAIRS:
+            d, outs = P.bfs_full(g, r, k, v)
+            np.testing.assert_array_equal(d, want, err_msg=f"{name} root={r} {k.name} {v.name}")
+            assert [o.new_frontier_count for o in outs] == cnt, (name, r, k, v)
+            assert all(o.elapsed_ns >= 1 for o in outs)
+
+
+@pytest.mark.parametrize("name", ["u1000", "kron10", "mesh64"])
+def test_push_warp_chunk_sizes(name):
+    g = graph(name)
+    r = G.roots(name)[1]
+    for chunk in (1, 2, 3, 5, 8, 16, 32, 33, 1000):
+        for v in P.CountVariant:
+            d, outs = P.bfs_full(g, r, P.KernelId.VERTEX_PUSH_WARP, v, chunk_size=chunk)
+            np.testing.assert_array_equal(d, G.depth(name, r))
+            assert [o.new_frontier_count for o in outs] == G.counts(name, r).tolist()
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if G.level_cases(n)])
+def test_level_contract_and_inconsistent_inputs(name):
+    """run_level on caller arrays (consistent partial rings and random
+    inconsistent arrays) mutates in place exactly like the reference."""
+    g = graph(name)
+    for arr, level, per_kernel in G.level_cases(name):
+        for k, (want, cnt) in enumerate(per_kernel):
+            for v in range(3):
+                d = arr.copy()
+                out = P.run_level(g, d, level, k, v)
+                np.testing.assert_array_equal(d, want, err_msg=f"{name} L{level} k{k} v{v}")
+                assert out.new_frontier_count == cnt
+            d64 = arr.astype(np.int64)
+            P.run_level(g, d64, level, k, 0)
+            np.testing.assert_array_equal(d64, want)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_adaptive_traces_match_reference(name):
+    g = graph(name)
+    tr = G.traces()["small"][name]
+    stats = P.compute_stats(g)
+    for r in G.roots(name):
+        for key, fname in G.trees_for(name):
+            flat = P.deserialize(G.tree_path(fname))
+            d, trace = P.adaptive_bfs(g, r, flat, stats)
+            np.testing.assert_array_equal(d, G.depth(name, r))
+            got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                   for x in trace.records]
+            assert got == tr[str(r)][key], (name, r, key)
+            assert all(x.elapsed_ns >= 1 and x.prediction_ns >= 1 for x in trace.records)
+            # the Python-policy path over the same device traversal agrees
+            d2, trace2 = P.adaptive_bfs(
+                g, r, lambda lvl, fv, f=flat: P.tree._class_to_result(f.predict_one(fv)), stats)
+            np.testing.assert_array_equal(d2, d)
+            assert trace2.pairs == trace.pairs
+            assert [x.fallback_used for x in trace2.records] == [x.fallback_used for x in trace.records]
+
+
+def test_fallback_chain_and_policies():
+    g = P.generate_graph("path", {"n": 6}, 0)
+    a, b = P.ALL_PAIRS[7], P.ALL_PAIRS[11]
+    _, tr = P.adaptive_bfs(g, 0, lambda lvl, f: {0: a, 2: b}.get(lvl, P.UNKNOWN))
+    assert tr.pairs[:4] == [a, a, b, b]
+    assert [r.fallback_used for r in tr.records][:4] == [False, True, False, True]
+    g = P.generate_graph("uniform-random", {"n": 60, "edges": 300}, 3)
+    d, tr = P.adaptive_bfs(g, 10, lambda lvl, f: P.pair_from_index((lvl * 7 + 3) % 15))
+    np.testing.assert_array_equal(d, P.reference_bfs(g, 10))
+    _, tr = P.adaptive_bfs(P.generate_graph("path", {"n": 8}, 0), 0, P.tree.leaf_tree(0))
+    assert tr.level_count == 8 and [r.frontier_size for r in tr.records] == [1] * 8
+
+
+def test_errors_match_reference():
+    g = graph("hand1")
+    with pytest.raises(ValueError, match="out of range"):
+        P.bfs_full(g, 6, 0, 0)
+    with pytest.raises(ValueError, match="out of range"):
+        P.init_depths(g, -1)
+    with pytest.raises(ValueError, match="chunk_size must be >= 1"):
+        P.bfs_full(g, 0, P.KernelId.VERTEX_PUSH_WARP, 0, chunk_size=0)
+    with pytest.raises(ValueError, match="unknown kernel"):
+        P.run_level(g, P.init_depths(g, 0), 0, 7, 0)
+    with pytest.raises(ValueError, match="unknown count variant"):
+        P.run_level(g, P.init_depths(g, 0), 0, 0, 5)
+    d = P.init_depths(g, 1)
+    assert d[1] == 0 and (np.delete(d, 1) == P.INF_DEPTH).all()
+
+
+def test_aggregate_count_device_variants():
+    rng = np.random.default_rng(7)
+    for size in [0, 1, 31, 32, 33, 1023, 1024, 1025, 100_000]:
+        c = rng.integers(0, 5, size=size)
+        for v in P.CountVariant:
+            assert P.aggregate_count(c, v) == int(c.sum())
+    big = rng.integers(0, 2**40, size=200)
+    assert P.aggregate_count(big, 2) == int(big.sum())
+
+
+@settings(max_examples=40)
+@given(data=st.data())
+def test_random_multigraphs_all_pairs(data):
+    n = data.draw(st.integers(1, 14))
+    pairs = data.draw(st.lists(st.tuples(st.integers(0, n - 1), st.integers(0, n - 1)),
+                               max_size=50))
+    g = P.build_combined(np.array(pairs, dtype=np.int64).reshape(-1, 2), n)
+    root = data.draw(st.integers(0, n - 1))
+    og = oracle.OracleGraph.from_graph(g)
+    want = oracle.reference_bfs(og, root)
+    hist = np.bincount(want[want != G.INF])
+    for k, v in P.ALL_PAIRS:
+        d, outs = P.bfs_full(g, root, k, v)
+        np.testing.assert_array_equal(d, want)
+        assert [o.new_frontier_count for o in outs[:-1]] == hist[1:].tolist()
+        assert outs[-1].new_frontier_count == 0
+
+
+@settings(max_examples=25)
+@given(data=st.data())
+def test_random_level_contract(data):
+    n = data.draw(st.integers(2, 12))
+    pairs = data.draw(st.lists(st.tuples(st.integers(0, n - 1), st.integers(0, n - 1)),
+                               min_size=1, max_size=40))
+    g = P.build_combined(np.array(pairs, dtype=np.int64), n)
+    root = data.draw(st.integers(0, n - 1))
+    og = oracle.OracleGraph.from_graph(g)
+    ref = oracle.reference_bfs(og, root)
+    level = data.draw(st.integers(0, int(ref[ref != G.INF].max())))
+    part = np.where(ref <= level, ref, G.INF).astype(np.int32)
+    for k in range(5):
+        for v in range(3):
+            d = part.copy()
+            out = P.run_level(g, d, level, k, v)
+            e = part.copy()
+            c, _ = oracle.run_level(og, e, level, k, v)
+            np.testing.assert_array_equal(d, e)
+            assert out.new_frontier_count == c
+
+
+def test_larger_random_graphs_vs_oracle():
+    rng = np.random.default_rng(20260819)
+    for n, m in ((800, 6000), (5000, 20000), (20000, 400000)):
+        g = P.build_combined(rng.integers(0, n, size=(m, 2)), n)
+        og = oracle.OracleGraph.from_graph(g)
+        stats = P.compute_stats(g)
+        flat = P.deserialize(G.tree_path("t1"))
+        for root in (0, n - 1, n // 3):
+            want = oracle.reference_bfs(og, root)
+            for k, v in P.ALL_PAIRS:
+                d, _ = P.bfs_full(g, root, k, v)
+                np.testing.assert_array_equal(d, want)
+            d, tr = P.adaptive_bfs(g, root, flat, stats)
+            np.testing.assert_array_equal(d, want)
+            _, orecs = oracle.adaptive_bfs(og, root, oracle.OracleTree(
+                P.features.canonical_indices(flat.selection), flat.features, flat.thresholds,
+                flat.lefts, flat.rights, flat.leaf_classes),
+                np.array([n, m, 0, 0, 0, 0, *P.features.static_vector(stats)[6:]]))
+            assert [(int(r.kernel), int(r.variant), r.fallback_used, r.frontier_size)
+                    for r in tr.records] == [(k_, v_, fb, fr) for (_, k_, v_, fb, fr, *_x) in orecs]
