@@ -169,6 +169,9 @@ ABFS_API int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree 
  * from after init_depths to the final count readback. */
 ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
 
+/* Number of kernels this traversal has launched (bench gpu_launches). */
+ABFS_API int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches);
+
 /* Sum over reached vertices of out-degree (GTEPS numerator basis). */
 ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices);
 

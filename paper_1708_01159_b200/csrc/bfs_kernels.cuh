@@ -11,6 +11,7 @@
 //   visited  u32 bitmap   bit v <=> depth[v] != INF (maintained exactly)
 //   fbm      u32 bitmap   current frontier (depth == level)   [bitmap form]
 //   q        u32 queue    current frontier vertex ids           [queue form]
+//   noin     u32 bitmap   in-degree 0 (static per graph; pull never scans them)
 // Top-down kernels emit the next frontier as a queue, pull emits a bitmap;
 // the engine converts between forms only when the next kernel needs the
 // other one (that conversion is the switching overhead).
@@ -21,6 +22,10 @@
 // caller depth arrays (run_level contract) set ctr->inconsistent and claims
 // fall back to atomicMin on the depth array, which reproduces _claim's
 // "lower to level+1, count only INF transitions" rule exactly.
+//
+// Level completion: the last CTA of a level's final kernel publishes the
+// counts into a host-mapped mailbox (seq-stamped), so the host learns the
+// level result without a memcpy or an event synchronisation.
 #pragma once
 
 #include "common.cuh"
@@ -38,6 +43,16 @@ struct Ctr {
     unsigned long long fcount;   // frontier size found by prepare
     unsigned long long reached_edges;
     unsigned long long reached_vertices;
+    unsigned int done;           // finished-CTA ticket of the publishing kernel
+    unsigned int pad;
+};
+
+// Host-mapped result of the last level (written by the device).
+struct Mailbox {
+    unsigned long long seq;
+    unsigned long long qlen;
+    unsigned long long count;
+    unsigned long long pad;
 };
 
 struct LevelCtx {
@@ -47,18 +62,28 @@ struct LevelCtx {
     uint32_t *q_next;            // next frontier queue (top-down)
     unsigned int *q_tail;        // = &ctr->qlen[out]
     unsigned long long *count;   // = &ctr->count[out] (pull)
+    unsigned int *units_tail;    // = &ctr->units[out] (heavy work units)
+    uint2 *units;
     const unsigned int *inconsistent;
     Ctr *ctr;
+    Mailbox *mb;                 // device view of the host mailbox
+    unsigned long long seq;
     int zero_slot;
     int32_t level;
     int32_t lvl1;
 };
 
 constexpr int kBlock = 256;
-constexpr int kQBuf = 2048;          // TWO_LEVEL CTA-local queue buffer
-constexpr int kEdgeTile = kBlock * 8; // edge slots per CTA (2 x uint4 per thread)
-constexpr uint32_t kHeavy = 2048;    // push-warp: degree above -> CTA units
-constexpr uint32_t kUnit = 4096;     // edges per CTA work unit
+constexpr int kWarps = kBlock / 32;
+constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
+constexpr int kEdgeVec = 4;           // uint4 loads in flight per thread (edge stream)
+constexpr int kEdgeTile = kBlock * 4 * kEdgeVec;  // slots per CTA iteration
+constexpr uint32_t kHeavy = 2048;     // push-warp: degree above -> CTA units
+constexpr uint32_t kUnit = 4096;      // edges per CTA work unit
+constexpr uint32_t kPullLight = 32;   // pull: per-lane scan up to this in-degree
+constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ void zero_slot(const LevelCtx &c) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -69,11 +94,31 @@ __device__ __forceinline__ void zero_slot(const LevelCtx &c) {
     }
 }
 
+// Last CTA to finish publishes (qlen, count) to the mapped mailbox.  Must be
+// reached by every thread of every CTA of the level's final kernel.
+__device__ __forceinline__ void publish(const LevelCtx &c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned ticket = atomicAdd(&c.ctr->done, 1u);
+        if (ticket == gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long q = atomicAdd(c.q_tail, 0u);
+            const unsigned long long n = atomicAdd(c.count, 0ull);
+            c.ctr->done = 0;
+            volatile Mailbox *mb = c.mb;
+            mb->qlen = q;
+            mb->count = n;
+            __threadfence_system();
+            mb->seq = c.seq;
+            __threadfence_system();
+        }
+    }
+}
+
 __device__ __forceinline__ bool in_bitmap(const uint32_t *bm, uint32_t v) {
     return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
 }
-
-__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // Could claiming v change anything?  (cheap filter before the atomic)
 __device__ __forceinline__ bool claim_possible(const LevelCtx &c, uint32_t v, bool consistent) {
@@ -106,8 +151,9 @@ __device__ __forceinline__ bool claim(const LevelCtx &c, uint32_t v, bool consis
 //   VAR 0 DIRECT_ATOMIC    one global atomic per discovery
 //   VAR 1 GROUP_REDUCE     warp ballot/popc, one global atomic per warp
 //   VAR 2 TWO_LEVEL_REDUCE warp ballot -> CTA shared-memory queue, one
-//                          global atomic per CTA (coalesced flush)
-// emit() must be called by all 32 lanes of a warp together.
+//                          global atomic per CTA flush (coalesced copy-out)
+// emit() must be called by all 32 lanes of a warp together; tile_end() and
+// finish() by all threads of the CTA.
 // ---------------------------------------------------------------------------
 struct SmemQ {
     unsigned int n;
@@ -164,14 +210,27 @@ struct QEmit {
         }
     }
 
-    // Must be reached by every thread of the CTA.
-    __device__ __forceinline__ void finish() {
-        if (VAR != 2) return;
-        __syncthreads();
+    __device__ __forceinline__ void flush() {
         const unsigned n = min(s->n, s->fail);
         if (threadIdx.x == 0) s->base = n ? atomicAdd(tail, n) : 0u;
         __syncthreads();
         for (unsigned i = threadIdx.x; i < n; i += blockDim.x) q[s->base + i] = s->buf[i];
+        __syncthreads();
+        if (threadIdx.x == 0) { s->n = 0; s->fail = 0xffffffffu; }
+        __syncthreads();
+    }
+
+    // Between block-uniform loop iterations: flush once half full.
+    __device__ __forceinline__ void tile_end() {
+        if (VAR != 2) return;
+        __syncthreads();
+        if (s->n >= (unsigned)kQBuf / 2) flush();
+    }
+
+    __device__ __forceinline__ void finish() {
+        if (VAR != 2) return;
+        __syncthreads();
+        flush();
     }
 };
 
@@ -208,8 +267,9 @@ struct CEmit {
 // ---------------------------------------------------------------------------
 // EDGE_LIST (run_level_edge_list + _relax_from_edges, kernels.py:196-219):
 // one item per forward slot e; active iff origins[e] is in the frontier;
-// relax destinations[e].  Origins stream with 128-bit evict-first loads;
-// destinations are gathered only for active slots.
+// relax destinations[e].  Persistent CTAs stream origins with four 128-bit
+// evict-first loads in flight per thread; destinations are gathered only
+// for active slots.
 // REV_EDGE_LIST (kernels.py:222-231): item per reverse slot f, head
 // sources[f], tail rev_owner[f].  The sorted tail stream is read first so
 // that sources[f] is gathered only when the claim could have an effect.
@@ -222,39 +282,62 @@ k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
     QEmit<VAR> em(&sq, c.q_next, c.q_tail);
     zero_slot(c);
     const bool consistent = (*c.inconsistent == 0);
-    const uint64_t tile = (uint64_t)blockIdx.x * kEdgeTile;
+    for (uint64_t tile = (uint64_t)blockIdx.x * kEdgeTile; tile < m;
+         tile += (uint64_t)gridDim.x * kEdgeTile) {
+        uint4 t4[kEdgeVec];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
-        uint32_t s4[4];
-        if (e + 4 <= m) {
-            const uint4 t = __ldcs(reinterpret_cast<const uint4 *>(stream_arr + e));
-            s4[0] = t.x; s4[1] = t.y; s4[2] = t.z; s4[3] = t.w;
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) s4[k] = (e + k < m) ? stream_arr[e + k] : 0u;
+        for (int h = 0; h < kEdgeVec; ++h) {
+            const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+            if (e + 4 <= m) {
+                t4[h] = __ldcs(reinterpret_cast<const uint4 *>(stream_arr + e));
+            } else {
+                t4[h].x = e + 0 < m ? stream_arr[e + 0] : 0u;
+                t4[h].y = e + 1 < m ? stream_arr[e + 1] : 0u;
+                t4[h].z = e + 2 < m ? stream_arr[e + 2] : 0u;
+                t4[h].w = e + 3 < m ? stream_arr[e + 3] : 0u;
+            }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            bool won = false;
-            uint32_t v = 0;
-            if (e + k < m) {
-                if (!REV) {
-                    if (in_bitmap(c.fbm, s4[k])) {
+        for (int h = 0; h < kEdgeVec; ++h) {
+            const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+            const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
+            bool act[4];
+            if (!REV) {
+                // origins are sorted: one frontier word usually covers all four
+                const uint32_t w0 = s4[0] >> 5, w3 = s4[3] >> 5;
+                if (w0 == w3) {
+                    const uint32_t fw = __ldg(c.fbm + w0);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) act[k] = (e + k < m) && ((fw >> (s4[k] & 31)) & 1u);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) act[k] = (e + k < m) && in_bitmap(c.fbm, s4[k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    act[k] = (e + k < m) && claim_possible(c, s4[k], consistent);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bool won = false;
+                uint32_t v = 0;
+                if (act[k]) {
+                    if (!REV) {
                         v = __ldg(gather_arr + e + k);
                         won = claim(c, v, consistent);
+                    } else {
+                        v = s4[k];
+                        if (in_bitmap(c.fbm, __ldg(gather_arr + e + k))) won = claim(c, v, consistent);
                     }
-                } else {
-                    v = s4[k];
-                    if (claim_possible(c, v, consistent) &&
-                        in_bitmap(c.fbm, __ldg(gather_arr + e + k)))
-                        won = claim(c, v, consistent);
                 }
+                em.emit(won, v);
             }
-            em.emit(won, v);
         }
+        em.tile_end();
     }
     em.finish();
+    publish(c);
 }
 
 // ---------------------------------------------------------------------------
@@ -287,8 +370,10 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
             }
             em.emit(won, v);
         }
+        em.tile_end();
     }
     em.finish();
+    publish(c);
 }
 
 // ---------------------------------------------------------------------------
@@ -301,19 +386,18 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
 template <int VAR, int VW>
 __global__ void __launch_bounds__(kBlock)
 k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
-            const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst,
-            uint2 *units, unsigned int *units_tail) {
+            const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
     QEmit<VAR> em(&sq, c.q_next, c.q_tail);
     zero_slot(c);
     const bool consistent = (*c.inconsistent == 0);
-    constexpr uint32_t per = 32 / VW;
+    constexpr uint32_t per = 32 / VW;               // frontier entries per warp step
+    constexpr uint32_t per_block = per * kWarps;
     const unsigned lane = lane_id();
     const uint32_t sub = lane / VW, sl = lane % VW;
-    const uint32_t warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * kBlock) >> 5;
-    for (uint32_t wb = warp * per; wb < F; wb += nwarps * per) {
-        const uint32_t i = wb + sub;
+    const uint32_t wib = threadIdx.x >> 5;
+    for (uint32_t bb = blockIdx.x * per_block; bb < F; bb += gridDim.x * per_block) {
+        const uint32_t i = bb + wib * per + sub;
         uint32_t j = 0, e = 0;
         if (i < F) {
             const uint32_t u = __ldg(q + i);
@@ -321,8 +405,8 @@ k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
             if (en - b > kHeavy) {
                 if (sl == 0) {
                     const uint32_t nu = (en - b + kUnit - 1) / kUnit;
-                    const uint32_t s = atomicAdd(units_tail, nu);
-                    for (uint32_t k = 0; k < nu; ++k) units[s + k] = make_uint2(u, k);
+                    const uint32_t s = atomicAdd(c.units_tail, nu);
+                    for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(u, k);
                 }
             } else {
                 j = b + sl;
@@ -339,21 +423,20 @@ k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
             }
             em.emit(won, v);
         }
+        em.tile_end();
     }
     em.finish();
 }
 
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
-k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off,
-        const uint32_t *__restrict__ dst, const uint2 *__restrict__ units,
-        const unsigned int *units_tail) {
+k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
     QEmit<VAR> em(&sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
-    const unsigned nunits = *units_tail;
+    const unsigned nunits = *(volatile unsigned *)c.units_tail;
     for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
-        const uint2 un = units[w];
+        const uint2 un = c.units[w];
         const uint32_t b = __ldg(out_off + un.x) + un.y * kUnit;
         const uint32_t e = min(__ldg(out_off + un.x + 1), b + kUnit);
         for (uint32_t jb = b; jb < e; jb += kBlock) {
@@ -366,59 +449,158 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off,
             }
             em.emit(won, v);
         }
+        em.tile_end();
     }
     em.finish();
+    publish(c);
 }
 
 // ---------------------------------------------------------------------------
-// VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): one warp per
-// 32-vertex bitmap word; each unvisited lane scans its in-neighbours in
-// order and stops at the first frontier vertex.  The warp owns its visited
-// and next-frontier words, so both are written without atomics, and every
-// next-frontier word is written (no clearing pass).
+// VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): unvisited
+// vertices scan their in-neighbours and stop at the first frontier vertex.
+// A warp takes a tile of 32 bitmap words; fully settled words (visited or
+// in-degree 0) cost one coalesced load and store.  For a word with work the
+// warp owns its 32 vertices:
+//   in-degree <= kPullLight   the lane scans its own list, 4 loads in flight
+//   <= kPullHeavy             the whole warp scans the list 128 at a time
+//   larger                    kUnit-edge CTA units (k_pull_heavy)
+// with early exit on the first frontier in-neighbour in every case.  The
+// warp owns its visited / next-frontier words, so they are written without
+// atomics, and every next-frontier word is written (no clearing pass).
 // ---------------------------------------------------------------------------
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
-       uint32_t *__restrict__ fbm_next, uint64_t n, uint64_t words) {
+       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t n,
+       uint64_t words) {
     __shared__ unsigned int sn;
     CEmit<VAR> em(&sn, c.count);
     zero_slot(c);
     const unsigned lane = lane_id();
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
-    for (uint64_t word = warp; word < words; word += nwarps) {
-        const uint32_t vis = c.visited[word];
-        const uint64_t v = word * 32 + lane;
-        const bool cand = v < n && !((vis >> lane) & 1u);
-        unsigned found_mask = 0;
-        if (__any_sync(kFull, cand)) {
+    for (uint64_t tile = warp; tile * 32 < words; tile += nwarps) {
+        const uint64_t myw = tile * 32 + lane;
+        uint32_t vis = 0xffffffffu, skip = 0xffffffffu;
+        if (myw < words) {
+            vis = c.visited[myw];
+            skip = vis | __ldg(noin + myw);
+        }
+        unsigned need = __ballot_sync(kFull, skip != 0xffffffffu);
+        if (myw < words && skip == 0xffffffffu) fbm_next[myw] = 0u;
+        while (need) {
+            const int wl = __ffs(need) - 1;
+            need &= need - 1;
+            const uint64_t word = tile * 32 + wl;
+            const uint32_t wvis = __shfl_sync(kFull, vis, wl);
+            const uint32_t wskip = __shfl_sync(kFull, skip, wl);
+            const uint64_t v = word * 32 + lane;
+            const bool cand = !((wskip >> lane) & 1u);   // padding bits are set in noin
             uint32_t j = 0, e = 0;
             if (cand) {
                 j = __ldg(in_off + v);
                 e = __ldg(in_off + v + 1);
             }
+            const bool light = cand && (e - j) <= kPullLight;
             bool found = false;
-            while (__any_sync(kFull, j < e)) {
-                if (j < e) {
-                    if (in_bitmap(c.fbm, __ldg(src + j))) {
+            // light lanes: own list, 4 independent loads per step
+            while (__any_sync(kFull, light && j < e)) {
+                if (light && j < e) {
+                    const uint32_t u0 = __ldg(src + j);
+                    const uint32_t u1 = j + 1 < e ? __ldg(src + j + 1) : u0;
+                    const uint32_t u2 = j + 2 < e ? __ldg(src + j + 2) : u0;
+                    const uint32_t u3 = j + 3 < e ? __ldg(src + j + 3) : u0;
+                    if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
+                        in_bitmap(c.fbm, u3)) {
                         found = true;
                         j = e;
                     } else {
-                        ++j;
+                        j += 4;
                     }
                 }
             }
-            found_mask = __ballot_sync(kFull, found);
+            // heavier lanes: cooperative warp scan, or CTA units
+            unsigned hm = __ballot_sync(kFull, cand && !light);
+            while (hm) {
+                const int l = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const uint32_t hj = __shfl_sync(kFull, j, l), he = __shfl_sync(kFull, e, l);
+                if (he - hj > kPullHeavy) {
+                    if (lane == 0) {
+                        const uint32_t nu = (he - hj + kUnit - 1) / kUnit;
+                        const uint32_t s = atomicAdd(c.units_tail, nu);
+                        for (uint32_t k = 0; k < nu; ++k)
+                            c.units[s + k] = make_uint2((uint32_t)(word * 32 + l), k);
+                    }
+                    continue;
+                }
+                bool f = false;
+                for (uint32_t b = hj; b < he; b += 128) {
+                    bool hit = false;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t x = b + k * 32 + lane;
+                        if (x < he) hit |= in_bitmap(c.fbm, __ldg(src + x));
+                    }
+                    if (__any_sync(kFull, hit)) {
+                        f = true;
+                        break;
+                    }
+                }
+                if (lane == (unsigned)l) found = f;
+            }
+            const unsigned fm = __ballot_sync(kFull, found);
             if (found) c.depth[v] = c.lvl1;
+            if (lane == 0) {
+                fbm_next[word] = fm;
+                if (fm) c.visited[word] = wvis | fm;
+            }
+            em.add(fm);
         }
-        if (lane == 0) {
-            fbm_next[word] = found_mask;
-            if (found_mask) c.visited[word] = vis | found_mask;
-        }
-        em.add(found_mask);
     }
     em.finish();
+}
+
+// CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
+// segment of one vertex's in-list with early exit; the first unit to find a
+// frontier in-neighbour claims the vertex (atomicOr on its visited bit).
+__global__ void __launch_bounds__(kBlock)
+k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
+             uint32_t *fbm_next) {
+    __shared__ int s_done;
+    const unsigned nunits = *(volatile unsigned *)c.units_tail;
+    for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
+        const uint2 un = c.units[w];
+        const uint32_t v = un.x, bit = 1u << (v & 31);
+        const uint32_t b = __ldg(in_off + v) + un.y * kUnit;
+        const uint32_t e = min(__ldg(in_off + v + 1), b + kUnit);
+        if (threadIdx.x == 0) s_done = (*(volatile uint32_t *)(c.visited + (v >> 5)) & bit) ? 1 : 0;
+        __syncthreads();
+        bool hit = false;
+        if (!s_done) {
+            for (uint32_t jb = b; jb < e; jb += kBlock * 4) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t x = jb + k * kBlock + threadIdx.x;
+                    if (x < e) hit |= in_bitmap(c.fbm, __ldg(src + x));
+                }
+                if (__syncthreads_or(hit)) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+        if (threadIdx.x == 0 && hit) {
+            const uint32_t old = atomicOr(c.visited + (v >> 5), bit);
+            if (!(old & bit)) {
+                c.depth[v] = c.lvl1;
+                atomicOr(fbm_next + (v >> 5), bit);
+                atomicAdd(c.count, 1ull);
+            }
+        }
+        __syncthreads();
+    }
+    publish(c);
 }
 
 // ---------------------------------------------------------------------------
@@ -429,7 +611,7 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
 __global__ void __launch_bounds__(kBlock)
 k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
                   unsigned int *cursor) {
-    __shared__ unsigned warp_tot[kBlock / 32];
+    __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned base;
     const uint64_t word = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     uint32_t w = word < words ? fbm[word] : 0u;
@@ -445,7 +627,7 @@ k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned acc = 0;
-        for (int i = 0; i < kBlock / 32; ++i) {
+        for (int i = 0; i < kWarps; ++i) {
             const unsigned t = warp_tot[i];
             warp_tot[i] = acc;
             acc += t;
@@ -491,6 +673,19 @@ __global__ void k_init(int32_t *depth, uint32_t *visited, uint32_t *fbm, uint32_
     }
     visited[word] = bits;
     fbm[word] = bits;
+}
+
+// noin: bit v set iff in-degree(v) == 0 or v >= n (padding).
+__global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, uint64_t words,
+                       uint32_t *noin) {
+    const uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (word >= words) return;
+    uint32_t bits = 0;
+    for (int k = 0; k < 32; ++k) {
+        const uint64_t v = word * 32 + k;
+        if (v >= n || in_off[v + 1] == in_off[v]) bits |= 1u << k;
+    }
+    noin[word] = bits;
 }
 
 // Rebuild frontier bitmap + visited bitmap from an arbitrary depth array.
@@ -543,7 +738,7 @@ k_reached(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_of
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_aggregate(const long long *__restrict__ counts, uint64_t n, unsigned long long *total) {
-    __shared__ unsigned long long part[kBlock / 32];
+    __shared__ unsigned long long part[kWarps];
     const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     unsigned long long x = i < n ? (unsigned long long)counts[i] : 0ull;
     if constexpr (VAR == 0) {
@@ -558,7 +753,7 @@ k_aggregate(const long long *__restrict__ counts, uint64_t n, unsigned long long
             __syncthreads();
             if (threadIdx.x == 0) {
                 unsigned long long s = 0;
-                for (int k = 0; k < kBlock / 32; ++k) s += part[k];
+                for (int k = 0; k < kWarps; ++k) s += part[k];
                 atomicAdd(total, s);
             }
         }

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "bfs_kernels.cuh"
 
@@ -36,11 +37,14 @@ struct abfs_traversal {
     bool own_stream = false;
     int32_t *depth = nullptr;
     uint32_t *visited = nullptr;
+    uint32_t *noin = nullptr;  // in-degree-0 bitmap (static)
     uint32_t *fbm[2] = {nullptr, nullptr};
     uint32_t *q[2] = {nullptr, nullptr};
     uint2 *units = nullptr;
     Ctr *dctr = nullptr;
     Ctr *hctr = nullptr;       // pinned
+    Mailbox *mb = nullptr;     // host-mapped level results
+    Mailbox *dmb = nullptr;    // device view of mb
     uint64_t words = 0;
     int cur = 0;
     bool has_q = false, has_bm = false;
@@ -48,8 +52,10 @@ struct abfs_traversal {
     int64_t expect_level = -1; // level whose frontier the state holds; -1 = rebuild
     uint64_t call = 0;
     bool inconsistent = false;
-    cudaEvent_t e0 = nullptr, e1 = nullptr, et0 = nullptr;
+    std::vector<cudaEvent_t> ev;  // 2 per level of the current traversal
+    cudaEvent_t et0 = nullptr;
     uint64_t last_trav_ns = 0;
+    uint64_t launches = 0;     // kernels launched by this traversal
 };
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
@@ -73,59 +79,110 @@ static inline unsigned grid_for(uint64_t items, uint64_t per_block, uint64_t cap
     return (unsigned)b;
 }
 
+// One full wave of resident CTAs for a persistent kernel (cached per kernel).
+template <typename K>
+static uint64_t persist_grid(K kernel) {
+    static uint64_t grid = 0;
+    if (!grid) {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kBlock, 0);
+        grid = (uint64_t)sms * (uint64_t)(per > 0 ? per : 1);
+    }
+    return grid;
+}
+
 template <int VAR>
-static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, int64_t chunk,
-                            int out) {
+static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, int64_t chunk) {
     const DevGraph &g = t->g->d;
     cudaStream_t s = t->stream;
     const uint32_t F = (uint32_t)t->F;
     switch (kernel) {
     case ABFS_EDGE_LIST:
-        k_edge<VAR, false><<<grid_for(g.m, kEdgeTile, 1ull << 31), kBlock, 0, s>>>(c, g.org, g.dst, g.m);
+        k_edge<VAR, false><<<grid_for(g.m, kEdgeTile, persist_grid(k_edge<VAR, false>)), kBlock, 0, s>>>(
+            c, g.org, g.dst, g.m);
+        t->launches += 1;
         break;
     case ABFS_REV_EDGE_LIST:
-        k_edge<VAR, true><<<grid_for(g.m, kEdgeTile, 1ull << 31), kBlock, 0, s>>>(c, g.rev_owner, g.src, g.m);
+        k_edge<VAR, true><<<grid_for(g.m, kEdgeTile, persist_grid(k_edge<VAR, true>)), kBlock, 0, s>>>(
+            c, g.rev_owner, g.src, g.m);
+        t->launches += 1;
         break;
     case ABFS_VERTEX_PUSH:
         k_push<VAR><<<grid_for(F, kBlock, 148 * 64), kBlock, 0, s>>>(c, t->q[t->cur], F, g.out_off, g.dst);
+        t->launches += 1;
         break;
     case ABFS_VERTEX_PULL:
-        k_pull<VAR><<<grid_for(t->words, kBlock / 32, 148 * 512), kBlock, 0, s>>>(
-            c, g.in_off, g.src, t->fbm[t->cur ^ 1], g.n, t->words);
+        k_pull<VAR><<<grid_for(t->words, kBlock, 148 * 64), kBlock, 0, s>>>(
+            c, g.in_off, g.src, t->noin, t->fbm[t->cur ^ 1], g.n, t->words);
+        k_pull_heavy<<<148 * 2, kBlock, 0, s>>>(c, g.in_off, g.src, t->fbm[t->cur ^ 1]);
+        t->launches += 2;
         break;
     default: {  // VERTEX_PUSH_WARP: nearest legal virtual-warp width <= chunk
         const int vw = chunk >= 32 ? 32 : chunk >= 16 ? 16 : chunk >= 8 ? 8 : chunk >= 4 ? 4 : chunk >= 2 ? 2 : 1;
-        const unsigned grid = grid_for((uint64_t)F * vw, kBlock, 148 * 64);
-        unsigned int *ut = &t->dctr->units[out];
+        const unsigned grid = grid_for((uint64_t)F * vw, kBlock, 148 * 32);
         const uint32_t *q = t->q[t->cur];
         switch (vw) {
-        case 32: k_push_warp<VAR, 32><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
-        case 16: k_push_warp<VAR, 16><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
-        case 8: k_push_warp<VAR, 8><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
-        case 4: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
-        case 2: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
-        default: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst, t->units, ut); break;
+        case 32: k_push_warp<VAR, 32><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 16: k_push_warp<VAR, 16><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 8: k_push_warp<VAR, 8><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 4: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 2: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        default: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
         }
-        k_heavy<VAR><<<148 * 4, kBlock, 0, s>>>(c, g.out_off, g.dst, t->units, ut);
+        k_heavy<VAR><<<148 * 2, kBlock, 0, s>>>(c, g.out_off, g.dst);
+        t->launches += 2;
     }
     }
 }
 
-// One level on the device-resident state.
+static int ensure_events(abfs_traversal *t, size_t n) {
+    while (t->ev.size() < n) {
+        cudaEvent_t e;
+        ABFS_CUDA(cudaEventCreate(&e));
+        t->ev.push_back(e);
+    }
+    return ABFS_OK;
+}
+
+// Wait for the level's mailbox stamp; poll the stream for faults.
+static int wait_mailbox(abfs_traversal *t, unsigned long long seq) {
+    volatile Mailbox *mb = t->mb;
+    for (uint64_t spin = 1;; ++spin) {
+        if (mb->seq == seq) return ABFS_OK;
+        if ((spin & 4095) == 0) {
+            cudaError_t e = cudaStreamQuery(t->stream);
+            if (e == cudaSuccess) {
+                if (mb->seq == seq) return ABFS_OK;
+                return fail(ABFS_ECUDA, "level completed without publishing its count");
+            }
+            if (e != cudaErrorNotReady)
+                return fail(ABFS_ECUDA, std::string("level kernel failed: ") + cudaGetErrorString(e));
+        }
+    }
+}
+
+// One level on the device-resident state.  ev_slot selects the event pair
+// bracketing the level; elapsed_ns is filled only when `timed_now` (else the
+// caller reads the events after the traversal).
 static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant, int64_t chunk,
-                      uint64_t *new_count, uint64_t *elapsed_ns, int *converted) {
+                      uint64_t *new_count, size_t ev_slot, bool timed_now, uint64_t *elapsed_ns,
+                      int *converted) {
     ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
     ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_TRY(ensure_events(t, 2 * ev_slot + 2));
     const DevGraph &g = t->g->d;
     cudaStream_t s = t->stream;
     int conv = 0;
-    ABFS_CUDA(cudaEventRecord(t->e0, s));
+    ABFS_CUDA(cudaEventRecord(t->ev[2 * ev_slot], s));
     if (t->expect_level != level) {
         // Frontier unknown for this level: rebuild from the depth array.
         ABFS_CUDA(cudaMemsetAsync(&t->dctr->inconsistent, 0, sizeof(unsigned), s));
         ABFS_CUDA(cudaMemsetAsync(&t->dctr->fcount, 0, sizeof(unsigned long long), s));
         k_prepare<<<grid_for(t->words, kBlock / 32, 148 * 512), kBlock, 0, s>>>(
             t->depth, g.n, t->words, (int32_t)level, t->fbm[t->cur], t->visited, t->dctr);
+        t->launches += 1;
         ABFS_CUDA(cudaGetLastError());
         ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, s));
         ABFS_CUDA(cudaStreamSynchronize(s));
@@ -140,17 +197,21 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     if (need_queue && !t->has_q) {
         k_bitmap_to_queue<<<grid_for(t->words, kBlock, 1ull << 31), kBlock, 0, s>>>(
             t->fbm[t->cur], t->words, t->q[t->cur], &t->dctr->cq);
+        t->launches += 1;
         t->has_q = true;
         conv = 1;
     } else if (!need_queue && !t->has_bm) {
         ABFS_CUDA(cudaMemsetAsync(t->fbm[t->cur], 0, t->words * 4, s));
-        if (t->F)
+        if (t->F) {
             k_queue_to_bitmap<<<grid_for(t->F, kBlock, 148 * 16), kBlock, 0, s>>>(
                 t->q[t->cur], (uint32_t)t->F, t->fbm[t->cur]);
+            t->launches += 1;
+        }
         t->has_bm = true;
         conv = 1;
     }
     const int out = (int)(t->call % 3);
+    const unsigned long long seq = ++t->call;
     LevelCtx c;
     c.depth = t->depth;
     c.visited = t->visited;
@@ -158,25 +219,25 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     c.q_next = t->q[t->cur ^ 1];
     c.q_tail = &t->dctr->qlen[out];
     c.count = &t->dctr->count[out];
+    c.units_tail = &t->dctr->units[out];
+    c.units = t->units;
     c.inconsistent = &t->dctr->inconsistent;
     c.ctr = t->dctr;
-    c.zero_slot = (int)((t->call + 1) % 3);
+    c.mb = t->dmb;
+    c.seq = seq;
+    c.zero_slot = (int)(seq % 3);
     c.level = (int32_t)level;
     c.lvl1 = (int32_t)(level + 1);
     switch (variant) {
-    case 0: launch_strategy<0>(t, c, kernel, chunk, out); break;
-    case 1: launch_strategy<1>(t, c, kernel, chunk, out); break;
-    default: launch_strategy<2>(t, c, kernel, chunk, out); break;
+    case 0: launch_strategy<0>(t, c, kernel, chunk); break;
+    case 1: launch_strategy<1>(t, c, kernel, chunk); break;
+    default: launch_strategy<2>(t, c, kernel, chunk); break;
     }
     ABFS_CUDA(cudaGetLastError());
-    ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, s));
-    ABFS_CUDA(cudaEventRecord(t->e1, s));
-    ABFS_CUDA(cudaEventSynchronize(t->e1));
-    float ms = 0.f;
-    ABFS_CUDA(cudaEventElapsedTime(&ms, t->e0, t->e1));
-    t->call++;
+    ABFS_CUDA(cudaEventRecord(t->ev[2 * ev_slot + 1], s));
+    ABFS_TRY(wait_mailbox(t, seq));
     const bool topdown = kernel != ABFS_VERTEX_PULL;
-    const uint64_t cnt = topdown ? (uint64_t)t->hctr->qlen[out] : (uint64_t)t->hctr->count[out];
+    const uint64_t cnt = topdown ? (uint64_t)t->mb->qlen : (uint64_t)t->mb->count;
     t->cur ^= 1;
     t->has_q = topdown;
     t->has_bm = !topdown;
@@ -185,9 +246,22 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     // depth level+1: the next level must rebuild its frontier from depths.
     t->expect_level = t->inconsistent ? -1 : level + 1;
     *new_count = cnt;
-    uint64_t ns = (uint64_t)llround((double)ms * 1e6);
-    *elapsed_ns = ns ? ns : 1;
+    if (timed_now) {
+        ABFS_CUDA(cudaEventSynchronize(t->ev[2 * ev_slot + 1]));
+        float ms = 0.f;
+        ABFS_CUDA(cudaEventElapsedTime(&ms, t->ev[2 * ev_slot], t->ev[2 * ev_slot + 1]));
+        const uint64_t ns = (uint64_t)llround((double)ms * 1e6);
+        *elapsed_ns = ns ? ns : 1;
+    }
     if (converted) *converted = conv;
+    return ABFS_OK;
+}
+
+static int event_ns(abfs_traversal *t, size_t slot, uint64_t *ns) {
+    float ms = 0.f;
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->ev[2 * slot], t->ev[2 * slot + 1]));
+    const uint64_t v = (uint64_t)llround((double)ms * 1e6);
+    *ns = v ? v : 1;
     return ABFS_OK;
 }
 
@@ -201,13 +275,14 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     t->words = (n + 31) / 32;
     const uint64_t wpad = t->words + 4;
     const uint64_t qcap = n + 4;
-    const uint64_t ucap = m / kHeavy + 64;
+    const uint64_t ucap = m / 2048 + 64;   // units of both heavy paths
     cudaError_t e = cudaSuccess;
     auto A = [&](void **p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
     };
     A((void **)&t->depth, (n + 4) * sizeof(int32_t));
     A((void **)&t->visited, wpad * 4);
+    A((void **)&t->noin, wpad * 4);
     A((void **)&t->fbm[0], wpad * 4);
     A((void **)&t->fbm[1], wpad * 4);
     A((void **)&t->q[0], qcap * 4);
@@ -215,13 +290,18 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     A((void **)&t->units, ucap * sizeof(uint2));
     A((void **)&t->dctr, sizeof(Ctr));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&t->hctr, sizeof(Ctr));
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&t->mb, sizeof(Mailbox), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&t->dmb, t->mb, 0);
+    if (e == cudaSuccess) std::memset(t->mb, 0, sizeof(Mailbox));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) t->own_stream = true;
-    if (e == cudaSuccess) e = cudaEventCreate(&t->e0);
-    if (e == cudaSuccess) e = cudaEventCreate(&t->e1);
     if (e == cudaSuccess) e = cudaEventCreate(&t->et0);
     if (e == cudaSuccess) e = cudaMemset(t->dctr, 0, sizeof(Ctr));
     if (e == cudaSuccess) e = cudaMemset(t->depth, 0xff, (n + 4) * sizeof(int32_t));
+    if (e == cudaSuccess && t->words) {
+        k_noin<<<grid_for(t->words, kBlock, 1ull << 31), kBlock>>>(g->d.in_off, n, t->words, t->noin);
+        e = cudaDeviceSynchronize();
+    }
     if (e != cudaSuccess) {
         set_error(std::string("traversal_create: ") + cudaGetErrorString(e));
         abfs_traversal_destroy(t);
@@ -237,6 +317,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     if (t->stream) cudaStreamSynchronize(t->stream);
     cudaFree(t->depth);
     cudaFree(t->visited);
+    cudaFree(t->noin);
     cudaFree(t->fbm[0]);
     cudaFree(t->fbm[1]);
     cudaFree(t->q[0]);
@@ -244,8 +325,8 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->units);
     cudaFree(t->dctr);
     if (t->hctr) cudaFreeHost(t->hctr);
-    if (t->e0) cudaEventDestroy(t->e0);
-    if (t->e1) cudaEventDestroy(t->e1);
+    if (t->mb) cudaFreeHost(t->mb);
+    for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
     if (t->et0) cudaEventDestroy(t->et0);
     if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
     delete t;
@@ -275,6 +356,7 @@ static int init_impl(abfs_traversal *t, int64_t root) {
     t->cur = 0;
     k_init<<<grid_for(t->words, kBlock, 1ull << 31), kBlock, 0, t->stream>>>(
         t->depth, t->visited, t->fbm[0], t->q[0], n, t->words, (uint32_t)root);
+    t->launches += 1;
     ABFS_CUDA(cudaGetLastError());
     ABFS_CUDA(cudaMemsetAsync(&t->dctr->inconsistent, 0, sizeof(unsigned), t->stream));
     t->has_q = true;
@@ -314,7 +396,7 @@ extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
 extern "C" int abfs_level(abfs_traversal *t, int64_t level, int kernel, int variant,
                           int64_t chunk, uint64_t *new_count, uint64_t *elapsed_ns) {
     if (!t || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
-    return level_impl(t, level, kernel, variant, chunk, new_count, elapsed_ns, nullptr);
+    return level_impl(t, level, kernel, variant, chunk, new_count, 0, true, elapsed_ns, nullptr);
 }
 
 extern "C" int abfs_run_level(abfs_traversal *t, int32_t *host, int64_t level, int kernel,
@@ -323,13 +405,14 @@ extern "C" int abfs_run_level(abfs_traversal *t, int32_t *host, int64_t level, i
     if (!t || !host || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
     ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
     ABFS_TRY(abfs_load_depths(t, host));
-    ABFS_TRY(level_impl(t, level, kernel, variant, chunk, new_count, elapsed_ns, nullptr));
+    ABFS_TRY(level_impl(t, level, kernel, variant, chunk, new_count, 0, true, elapsed_ns, nullptr));
     return abfs_read_depths(t, host);
 }
 
-static int finish_traversal(abfs_traversal *t, int32_t *depths_out) {
+static int finish_traversal(abfs_traversal *t, size_t n_levels, int32_t *depths_out) {
+    ABFS_CUDA(cudaEventSynchronize(t->ev[2 * (n_levels - 1) + 1]));
     float ms = 0.f;
-    ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->e1));
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->ev[2 * (n_levels - 1) + 1]));
     t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
     if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
     return ABFS_OK;
@@ -342,19 +425,22 @@ extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int va
     ABFS_TRY(level_params_ok(0, kernel, variant, chunk));
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
+    size_t nl = 0;
     for (int64_t level = 0;; ++level) {
-        uint64_t c = 0, el = 0;
-        ABFS_TRY(level_impl(t, level, kernel, variant, chunk, &c, &el, nullptr));
-        if ((size_t)level < cap) {
-            if (counts) counts[level] = c;
-            if (elapsed) elapsed[level] = el;
-        }
+        uint64_t c = 0;
+        ABFS_TRY(level_impl(t, level, kernel, variant, chunk, &c, (size_t)level, false, nullptr,
+                            nullptr));
+        if ((size_t)level < cap && counts) counts[level] = c;
         if (c == 0) {
-            *n_levels = (size_t)level + 1;
+            nl = (size_t)level + 1;
             break;
         }
     }
-    return finish_traversal(t, depths_out);
+    *n_levels = nl;
+    ABFS_TRY(finish_traversal(t, nl, depths_out));
+    if (elapsed)
+        for (size_t l = 0; l < nl && l < cap; ++l) ABFS_TRY(event_ns(t, l, &elapsed[l]));
+    return ABFS_OK;
 }
 
 extern "C" int abfs_features(const double *static24, uint64_t frontier, uint64_t discovered,
@@ -439,9 +525,9 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
             pk = cls / 3;
             pv = cls % 3;
         }
-        uint64_t c = 0, el = 0;
+        uint64_t c = 0;
         int conv = 0;
-        ABFS_TRY(level_impl(t, level, pk, pv, chunk, &c, &el, &conv));
+        ABFS_TRY(level_impl(t, level, pk, pv, chunk, &c, (size_t)level, false, nullptr, &conv));
         if (recs && (size_t)level < cap) {
             abfs_level_record &r = recs[level];
             r.level = level;
@@ -451,7 +537,7 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
             r.converted = conv;
             r.frontier_size = frontier;
             r.new_count = c;
-            r.elapsed_ns = el;
+            r.elapsed_ns = 0;   // filled from the level's events after the traversal
             r.prediction_ns = pred ? pred : 1;
         }
         if (c == 0) {
@@ -461,7 +547,16 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
         frontier = c;
         discovered += c;
     }
-    return finish_traversal(t, depths_out);
+    ABFS_TRY(finish_traversal(t, *n_levels, depths_out));
+    if (recs)
+        for (size_t l = 0; l < *n_levels && l < cap; ++l) ABFS_TRY(event_ns(t, l, &recs[l].elapsed_ns));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches) {
+    if (!t || !launches) return fail(ABFS_EINVAL, "null argument");
+    *launches = t->launches;
+    return ABFS_OK;
 }
 
 extern "C" int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns) {
@@ -475,6 +570,7 @@ extern "C" int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *
     ABFS_CUDA(cudaSetDevice(t->device));
     ABFS_CUDA(cudaMemsetAsync(&t->dctr->reached_edges, 0, 16, t->stream));
     k_reached<<<148 * 8, kBlock, 0, t->stream>>>(t->depth, t->g->d.out_off, t->g->d.n, t->dctr);
+    t->launches += 1;
     ABFS_CUDA(cudaGetLastError());
     ABFS_CUDA(cudaMemcpyAsync(t->hctr, t->dctr, sizeof(Ctr), cudaMemcpyDeviceToHost, t->stream));
     ABFS_CUDA(cudaStreamSynchronize(t->stream));
