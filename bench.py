@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""bench.py -- tree-switched BFS GTEPS, Kronecker scale 24, B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Kronecker scale 24, edgefactor 16,
+symmetrised (rmat-like a,b,c = .57/.19/.19, seed 1, generated bit-exactly on
+the device), tree-switched BFS from 64 seeded non-isolated roots.  A step =
+one tree-switched BFS from each of --roots-per-step roots (rotating through
+the 64).  GTEPS = Σ_roots (Σ out-degree of reached vertices / 2) / device time
+of the K timed steps (CUDA events on the traversal's stream, init_depths
+included).  The graph (8.1 GB of arrays) is larger than L2 and stays
+resident, like model weights.
+
+With N > 1 ranks each GPU holds the graph and takes its own share of the
+roots (multi-source sharding, no data-path collective): scaling "weak".
+
+`--impl reference` times the reference algorithm's CPU port (oracle/, C +
+OpenMP, all host cores) on the same config: the reference is pure Python +
+numpy and cannot travel to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BFS GTEPS (Kronecker scale 24, 1/2/4/8 B200); HBM GB/s vs peak"
+UNIT = "GTEPS"
+HBM_FALLBACK = 6650.0
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def pick_roots(out_offsets, k=64, seed=1):
+    deg = np.diff(out_offsets.astype(np.int64))
+    cand = np.flatnonzero(deg > 0)
+    rng = np.random.default_rng(seed)
+    return sorted(int(x) for x in rng.choice(cand, size=min(k, cand.size), replace=False))
+
+
+def default_model():
+    for p in ("models/gpu_tree.tree", "tests/golden/trees/t1.tree"):
+        q = os.path.join(ROOT, p)
+        if os.path.exists(q):
+            return q
+    raise FileNotFoundError("no tree model")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# Work model: algorithmic bytes of one level.
+# ---------------------------------------------------------------------------
+def level_bytes(kernel, V, E, F, N, EF, U, A_rev, ES, converted):
+    bm = (V + 7) // 8
+    if kernel in (0,):
+        b = 4 * E + 4 * EF + 4 * N + 2 * bm
+    elif kernel == 1:
+        b = 4 * E + 4 * A_rev + 4 * N + 2 * bm
+    elif kernel in (2, 4):
+        b = 4 * F + 8 * F + 4 * EF + 4 * N + 4 * N + bm
+    else:
+        b = bm + 8 * U + 4 * ES + bm + 4 * N
+    if converted:
+        b += bm + 4 * F
+    return b
+
+
+def work_model(t, records, V, E):
+    """Per-level (kernel, ns, bytes) from one instrumented replay."""
+    nlev = len(records)
+    st = t.level_stats(nlev)
+    cnt, od, idg, es = st["count"], st["out_deg"], st["in_deg"], st["scanned"]
+    out = []
+    discovered = 0
+    unvisited_in = int(idg.sum())
+    for lvl, r in enumerate(records):
+        F = int(cnt[lvl])
+        N = int(cnt[lvl + 1]) if lvl + 1 < nlev else 0
+        discovered += F
+        unvisited_in -= int(idg[lvl])
+        U = V - discovered
+        b = level_bytes(int(r.kernel), V, E, F, N, int(od[lvl]), U, unvisited_in,
+                        int(es[lvl]), bool(r.converted))
+        out.append((int(r.kernel), int(r.variant), int(r.elapsed_ns), b))
+    return out
+
+
+KERNEL_NAMES = ["EDGE_LIST", "REV_EDGE_LIST", "VERTEX_PUSH", "VERTEX_PULL", "VERTEX_PUSH_WARP"]
+
+
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1708_01159_b200 as P
+    from paper_1708_01159_b200 import DeviceGraph, Traversal
+    from paper_1708_01159_b200.features import static_vector
+
+    rank, world, local = env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+
+    t_setup = time.time()
+    dg = DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev)
+    V, E = dg.vertex_count, dg.edge_count
+    oo, io = dg.offsets()
+    stats = P.compute_stats(dg)
+    static24 = static_vector(stats)
+    roots_all = pick_roots(oo, 64, seed=1)
+    my_roots = roots_all[rank::world] if world > 1 else roots_all
+    flat = P.deserialize(a.model)
+    tree = flat.as_abfs()
+    trav = Traversal(dg)
+    stream = torch.cuda.Stream(device=dev)
+    trav.set_stream(stream.cuda_stream)
+
+    # traversed edges per root (Graph500 undirected basis: Σ out-degree / 2)
+    m_trav = {}
+    for r in my_roots:
+        trav.adaptive(r, tree, static24, 32)
+        e, _ = trav.reached()
+        m_trav[r] = e / 2
+    setup_s = time.time() - t_setup
+
+    R = a.roots_per_step
+    order = [my_roots[i % len(my_roots)] for i in range(R * (a.warmup + a.steps))]
+    for s in range(a.warmup):
+        for r in order[s * R:(s + 1) * R]:
+            trav.adaptive(r, tree, static24, 32)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = trav.launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    edges = 0.0
+    bfs_ns = 0
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for s in range(a.warmup, a.warmup + a.steps):
+            for r in order[s * R:(s + 1) * R]:
+                trav.adaptive(r, tree, static24, 32)
+                bfs_ns += trav.last_ns()
+                edges += m_trav[r]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = trav.launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        ee = torch.tensor([edges], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ee)
+        edges = float(ee.item())
+    gteps = edges / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (instrumented replay, untimed) ----
+    peak, peak_kind = measured_peak_hbm()
+    per_kernel = {}
+    trav.instrument(True)
+    for r in my_roots[:R]:
+        recs = trav.adaptive(r, tree, static24, 32)
+        for k, v, ns, b in work_model(trav, recs, V, E):
+            agg = per_kernel.setdefault(k, [0, 0, 0])
+            agg[0] += ns
+            agg[1] += b
+            agg[2] += 1
+    trav.instrument(False)
+    # per-level times of the (uninstrumented) switched run for the same roots
+    lv_ns = {}
+    trace_pairs = None
+    for r in my_roots[:R]:
+        recs = trav.adaptive(r, tree, static24, 32)
+        trace_pairs = trace_pairs or [(KERNEL_NAMES[x.kernel], x.variant) for x in recs]
+        for x in recs:
+            lv_ns[x.kernel] = lv_ns.get(x.kernel, 0) + x.elapsed_ns
+    dom = max(per_kernel, key=lambda k: lv_ns.get(k, 0))
+    dom_ns = lv_ns[dom]
+    dom_bytes = per_kernel[dom][1]
+    achieved = dom_bytes / (dom_ns * 1e-9) / 1e9
+    total_ns = sum(lv_ns.values())
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as fh:
+                traffic = json.load(fh).get(KERNEL_NAMES[dom])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "kernel": KERNEL_NAMES[dom],
+                "kernel_share_of_step": round(dom_ns / total_ns, 3),
+                "launches_measured": per_kernel[dom][2],
+                "algorithmic_bytes": int(dom_bytes),
+                "whole_traversal_GBps": round(sum(v[1] for v in per_kernel.values()) /
+                                              (total_ns * 1e-9) / 1e9, 1)}
+
+    # ---- e2e through the public API with host results ----------------------
+    e2e = None
+    if rank == 0 or world > 1:
+        dg_api = dg
+        dg_api._scratch = Traversal(dg)
+        n_e2e = min(len(my_roots), R * max(1, a.steps // 2))
+        for r in my_roots[:2]:
+            P.adaptive_bfs(dg_api, r, flat, stats)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_edges = 0.0
+        for i in range(n_e2e):
+            r = my_roots[i % len(my_roots)]
+            depths, _ = P.adaptive_bfs(dg_api, r, flat, stats)
+            e_edges += m_trav[r]
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        e2e = {"value": round(e_edges / el / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(R * 8 + flat.node_count * 19 + 24 * 8),
+               "d2h_bytes_per_step": int(R * 4 * V),
+               "api": "paper_1708_01159_b200.adaptive_bfs(graph, root, FlatTree, stats) -> host int32 depths",
+               "bfs_per_sample": n_e2e}
+
+    # ---- CPU baseline: oracle port of the reference algorithm --------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(dg, roots_all, a.model, static24, a.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator)",
+            "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
+                       "scale": a.scale, "vertices": V, "directed_edge_slots": E,
+                       "roots_per_step": R, "roots_pool": 64,
+                       "model": os.path.relpath(a.model, ROOT),
+                       "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
+                       "l2": "inputs larger than L2 (graph arrays 8.1 GB)"},
+            "gteps_graph500_tbfs": round(edges / (bfs_ns * 1e-9) / 1e9, 3) if world == 1 else None,
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "trace_first_root": trace_pairs,
+            "setup_s": round(setup_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(dg, roots, model, static24, budget_s):
+    """The reference algorithm's CPU port (oracle/) on the host cores, same
+    graph / tree / roots, bounded to ~budget_s seconds (>= 1 root)."""
+    import oracle
+    import paper_1708_01159_b200 as P
+    from paper_1708_01159_b200.features import canonical_indices
+
+    a = dg.download(rev_owner=True)
+    og = oracle.OracleGraph(dg.vertex_count, dg.edge_count, a["out_offsets"], a["destinations"],
+                            a["origins"], a["in_offsets"], a["sources"], a["rev_owner"])
+    del a
+    flat = P.deserialize(model)
+    ot = oracle.OracleTree(canonical_indices(flat.selection), flat.features, flat.thresholds,
+                           flat.lefts, flat.rights, flat.leaf_classes)
+    threads = os.cpu_count() or 1
+    deg = np.diff(og.out_offsets.astype(np.int64))
+    done, edges, el = 0, 0.0, 0.0
+    for r in roots:
+        t0 = time.perf_counter()
+        d, _ = oracle.adaptive_bfs(og, r, ot, static24, threads=threads)
+        el += time.perf_counter() - t0
+        edges += deg[d != 2**31 - 1].sum() / 2
+        done += 1
+        if el >= budget_s:
+            break
+    return {"value": round(edges / el / 1e9, 5), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{done} tree-switched BFS root(s) on the full K{int(np.log2(dg.vertex_count))} "
+                      f"graph, same tree; C+OpenMP port of the reference level kernels "
+                      f"(oracle/abfs_oracle.c), {el:.1f}s wall"}
+
+
+def run_reference(a):
+    """--impl reference: the reference algorithm's CPU port, rank 0 only."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    import paper_1708_01159_b200.graph as G
+    from paper_1708_01159_b200.features import canonical_indices, static_vector
+    from paper_1708_01159_b200.tree import deserialize
+
+    t0 = time.time()
+    threads = os.cpu_count() or 1
+    src, dst = oracle.generate_rmat_pairs(a.scale, 16 << a.scale, 1, threads=threads)
+    og = oracle.build_combined(1 << a.scale, np.concatenate([src, dst]), np.concatenate([dst, src]))
+    del src, dst
+    stats = G.stats_from_offsets(og.n, og.m, og.out_offsets, og.in_offsets)
+    static24 = static_vector(stats)
+    roots = pick_roots(og.out_offsets, 64, seed=1)
+    flat = deserialize(a.model)
+    ot = oracle.OracleTree(canonical_indices(flat.selection), flat.features, flat.thresholds,
+                           flat.lefts, flat.rights, flat.leaf_classes)
+    deg = np.diff(og.out_offsets.astype(np.int64))
+    setup = time.time() - t0
+    vals, times = [], []
+    edges_tot, el_tot = 0.0, 0.0
+    for s in range(a.warmup + a.steps):
+        r = roots[s % len(roots)]
+        t1 = time.perf_counter()
+        d, _ = oracle.adaptive_bfs(og, r, ot, static24, threads=threads)
+        el = time.perf_counter() - t1
+        if s >= a.warmup:
+            e = deg[d != 2**31 - 1].sum() / 2
+            edges_tot += e
+            el_tot += el
+            times.append(el)
+    gteps = edges_tot / el_tot / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(gteps, 5), "unit": UNIT,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(1e3 * el_tot / max(1, a.steps), 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (host-generated Kronecker, same generator/seed)",
+            "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
+                       "scale": a.scale, "roots_per_step": 1,
+                       "model": os.path.relpath(a.model, ROOT)},
+            "cpu_baseline": {"value": round(gteps, 5), "unit": UNIT, "cores": threads,
+                             "kind": "port",
+                             "sample": f"1 tree-switched BFS per step ({a.steps} steps) on the "
+                                       f"full graph; C+OpenMP port of the reference kernels"},
+            "e2e": {"value": round(gteps, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "setup_s": round(setup, 1)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--roots-per-step", type=int, default=4)
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    a = ap.parse_args()
+    a.model = os.path.abspath(a.model) if a.model else default_model()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

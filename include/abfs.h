@@ -172,6 +172,15 @@ ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
 /* Number of kernels this traversal has launched (bench gpu_launches). */
 ABFS_API int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches);
 
+/* Work-model instrumentation (bench roofline, not on the timed path):
+ * when on, pull levels count the in-edges they scan (ES). */
+ABFS_API int abfs_traversal_instrument(abfs_traversal *t, int on);
+/* Per-depth histograms of the current depth array: count, Σ out-degree,
+ * Σ in-degree for depths 0..nlev-1 and slot nlev = unreached (each array
+ * nlev+1 long); scanned[l] = ES of level l from the last instrumented run. */
+ABFS_API int abfs_traversal_level_stats(abfs_traversal *t, size_t nlev, uint64_t *count,
+                                        uint64_t *out_deg, uint64_t *in_deg, uint64_t *scanned);
+
 /* Sum over reached vertices of out-degree (GTEPS numerator basis). */
 ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices);
 

@@ -77,6 +77,9 @@ _SIGNATURES = {
                                          ctypes.POINTER(ctypes.c_size_t)]),
     "abfs_last_traversal_ns": (ctypes.c_int, [ctypes.c_void_p, u64p]),
     "abfs_traversal_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),
+    "abfs_traversal_instrument": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "abfs_traversal_level_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, u64p, u64p,
+                                                  u64p, u64p]),
     "abfs_reached_edges": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p]),
     "abfs_aggregate_count": (ctypes.c_int, [ctypes.c_int, i64p, ctypes.c_size_t, ctypes.c_int,
                                             i64p]),

@@ -67,6 +67,7 @@ struct LevelCtx {
     const unsigned int *inconsistent;
     Ctr *ctr;
     Mailbox *mb;                 // device view of the host mailbox
+    unsigned long long *es;      // optional: in-edges scanned by pull (instrumented runs)
     unsigned long long seq;
     int zero_slot;
     int32_t level;
@@ -297,41 +298,51 @@ k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
                 t4[h].w = e + 3 < m ? stream_arr[e + 3] : 0u;
             }
         }
+        bool act[kEdgeVec][4];
+        bool any = false;
 #pragma unroll
         for (int h = 0; h < kEdgeVec; ++h) {
             const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
             const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
-            bool act[4];
             if (!REV) {
                 // origins are sorted: one frontier word usually covers all four
                 const uint32_t w0 = s4[0] >> 5, w3 = s4[3] >> 5;
                 if (w0 == w3) {
                     const uint32_t fw = __ldg(c.fbm + w0);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) act[k] = (e + k < m) && ((fw >> (s4[k] & 31)) & 1u);
+                    for (int k = 0; k < 4; ++k) act[h][k] = (e + k < m) && ((fw >> (s4[k] & 31)) & 1u);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) act[k] = (e + k < m) && in_bitmap(c.fbm, s4[k]);
+                    for (int k = 0; k < 4; ++k) act[h][k] = (e + k < m) && in_bitmap(c.fbm, s4[k]);
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    act[k] = (e + k < m) && claim_possible(c, s4[k], consistent);
+                    act[h][k] = (e + k < m) && claim_possible(c, s4[k], consistent);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                bool won = false;
-                uint32_t v = 0;
-                if (act[k]) {
-                    if (!REV) {
-                        v = __ldg(gather_arr + e + k);
-                        won = claim(c, v, consistent);
-                    } else {
-                        v = s4[k];
-                        if (in_bitmap(c.fbm, __ldg(gather_arr + e + k))) won = claim(c, v, consistent);
+            for (int k = 0; k < 4; ++k) any |= act[h][k];
+        }
+        if (__any_sync(kFull, any)) {  // idle warps skip the claim/emit stage
+#pragma unroll
+            for (int h = 0; h < kEdgeVec; ++h) {
+                const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+                const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    bool won = false;
+                    uint32_t v = 0;
+                    if (act[h][k]) {
+                        if (!REV) {
+                            v = __ldg(gather_arr + e + k);
+                            won = claim(c, v, consistent);
+                        } else {
+                            v = s4[k];
+                            if (in_bitmap(c.fbm, __ldg(gather_arr + e + k))) won = claim(c, v, consistent);
+                        }
                     }
+                    em.emit(won, v);
                 }
-                em.emit(won, v);
             }
         }
         em.tile_end();
@@ -461,9 +472,9 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // A warp takes a tile of 32 bitmap words; fully settled words (visited or
 // in-degree 0) cost one coalesced load and store.  For a word with work the
 // warp owns its 32 vertices:
-//   in-degree <= kPullLight   the lane scans its own list, 4 loads in flight
-//   <= kPullHeavy             the whole warp scans the list 128 at a time
-//   larger                    kUnit-edge CTA units (k_pull_heavy)
+//   first kPullLight entries  every lane scans its own list, 4 loads in flight
+//   rest <= kPullHeavy        the whole warp scans the list 128 at a time
+//   rest larger               kUnit-edge CTA units (k_pull_heavy)
 // with early exit on the first frontier in-neighbour in every case.  The
 // warp owns its visited / next-frontier words, so they are written without
 // atomics, and every next-frontier word is written (no clearing pass).
@@ -479,6 +490,7 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
     const unsigned lane = lane_id();
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+    unsigned long long scanned = 0;
     for (uint64_t tile = warp; tile * 32 < words; tile += nwarps) {
         const uint64_t myw = tile * 32 + lane;
         uint32_t vis = 0xffffffffu, skip = 0xffffffffu;
@@ -501,26 +513,28 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
                 j = __ldg(in_off + v);
                 e = __ldg(in_off + v + 1);
             }
-            const bool light = cand && (e - j) <= kPullLight;
+            // phase A (every candidate): own list, 4 independent loads per
+            // step, at most kPullLight entries -- most vertices stop here
+            const uint32_t ja = min(e, j + kPullLight);
             bool found = false;
-            // light lanes: own list, 4 independent loads per step
-            while (__any_sync(kFull, light && j < e)) {
-                if (light && j < e) {
+            while (__any_sync(kFull, j < ja)) {
+                if (j < ja) {
+                    scanned += min(4u, ja - j);
                     const uint32_t u0 = __ldg(src + j);
-                    const uint32_t u1 = j + 1 < e ? __ldg(src + j + 1) : u0;
-                    const uint32_t u2 = j + 2 < e ? __ldg(src + j + 2) : u0;
-                    const uint32_t u3 = j + 3 < e ? __ldg(src + j + 3) : u0;
+                    const uint32_t u1 = j + 1 < ja ? __ldg(src + j + 1) : u0;
+                    const uint32_t u2 = j + 2 < ja ? __ldg(src + j + 2) : u0;
+                    const uint32_t u3 = j + 3 < ja ? __ldg(src + j + 3) : u0;
                     if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
                         in_bitmap(c.fbm, u3)) {
                         found = true;
                         j = e;
                     } else {
-                        j += 4;
+                        j = min(j + 4, ja);
                     }
                 }
             }
             // heavier lanes: cooperative warp scan, or CTA units
-            unsigned hm = __ballot_sync(kFull, cand && !light);
+            unsigned hm = __ballot_sync(kFull, cand && !found && j < e);
             while (hm) {
                 const int l = __ffs(hm) - 1;
                 hm &= hm - 1;
@@ -536,6 +550,7 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
                 }
                 bool f = false;
                 for (uint32_t b = hj; b < he; b += 128) {
+                    scanned += (lane == 0) ? min(128u, he - b) : 0u;
                     bool hit = false;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -559,6 +574,11 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
         }
     }
     em.finish();
+    if (c.es) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) scanned += __shfl_down_sync(kFull, scanned, o);
+        if (lane == 0 && scanned) atomicAdd(c.es, scanned);
+    }
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
@@ -579,6 +599,7 @@ k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__
         bool hit = false;
         if (!s_done) {
             for (uint32_t jb = b; jb < e; jb += kBlock * 4) {
+                if (c.es && threadIdx.x == 0) atomicAdd(c.es, (unsigned long long)min(kBlock * 4u, e - jb));
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const uint32_t x = jb + k * kBlock + threadIdx.x;
@@ -732,6 +753,40 @@ k_reached(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_of
         atomicAdd(&ctr->reached_edges, e);
         atomicAdd(&ctr->reached_vertices, r);
     }
+}
+
+// Per-depth histograms for the work model (bench roofline): for each depth
+// d < nlev: vertex count, Σ out-degree, Σ in-degree; slot nlev = unreached.
+__global__ void __launch_bounds__(kBlock)
+k_level_hist(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_off,
+             const uint32_t *__restrict__ in_off, uint64_t n, uint32_t nlev,
+             unsigned long long *hist /* 3 * (nlev + 1) */) {
+    __shared__ unsigned long long sh[3 * 65];
+    const bool local = nlev < 64;
+    for (int i = threadIdx.x; i < 3 * 65; i += kBlock) sh[i] = 0;
+    __syncthreads();
+    for (uint64_t v = (uint64_t)blockIdx.x * kBlock + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * kBlock) {
+        const int32_t d = depth[v];
+        const uint32_t slot = (d == kInf || d < 0 || (uint32_t)d >= nlev) ? nlev : (uint32_t)d;
+        const unsigned long long od = out_off[v + 1] - out_off[v], id = in_off[v + 1] - in_off[v];
+        if (local) {
+            atomicAdd(&sh[slot], 1ull);
+            atomicAdd(&sh[65 + slot], od);
+            atomicAdd(&sh[130 + slot], id);
+        } else {
+            atomicAdd(&hist[slot], 1ull);
+            atomicAdd(&hist[(nlev + 1) + slot], od);
+            atomicAdd(&hist[2 * (nlev + 1) + slot], id);
+        }
+    }
+    __syncthreads();
+    if (local)
+        for (uint32_t i = threadIdx.x; i <= nlev; i += kBlock) {
+            if (sh[i]) atomicAdd(&hist[i], sh[i]);
+            if (sh[65 + i]) atomicAdd(&hist[(nlev + 1) + i], sh[65 + i]);
+            if (sh[130 + i]) atomicAdd(&hist[2 * (nlev + 1) + i], sh[130 + i]);
+        }
 }
 
 // aggregate_count on the device with the three reduction shapes.

@@ -56,6 +56,9 @@ struct abfs_traversal {
     cudaEvent_t et0 = nullptr;
     uint64_t last_trav_ns = 0;
     uint64_t launches = 0;     // kernels launched by this traversal
+    unsigned long long *des = nullptr;   // pull scanned-edge counter (instrumented)
+    bool instrument = false;
+    std::vector<uint64_t> es_log;        // per level (instrumented runs)
 };
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
@@ -224,6 +227,11 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     c.inconsistent = &t->dctr->inconsistent;
     c.ctr = t->dctr;
     c.mb = t->dmb;
+    c.es = nullptr;
+    if (t->instrument) {
+        ABFS_CUDA(cudaMemsetAsync(t->des, 0, sizeof(unsigned long long), s));
+        c.es = t->des;
+    }
     c.seq = seq;
     c.zero_slot = (int)(seq % 3);
     c.level = (int32_t)level;
@@ -246,6 +254,13 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     // depth level+1: the next level must rebuild its frontier from depths.
     t->expect_level = t->inconsistent ? -1 : level + 1;
     *new_count = cnt;
+    if (t->instrument) {
+        unsigned long long es = 0;
+        ABFS_CUDA(cudaMemcpyAsync(&es, t->des, sizeof(es), cudaMemcpyDeviceToHost, s));
+        ABFS_CUDA(cudaStreamSynchronize(s));
+        if (t->es_log.size() <= ev_slot) t->es_log.resize(ev_slot + 1);
+        t->es_log[ev_slot] = es;
+    }
     if (timed_now) {
         ABFS_CUDA(cudaEventSynchronize(t->ev[2 * ev_slot + 1]));
         float ms = 0.f;
@@ -289,6 +304,7 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     A((void **)&t->q[1], qcap * 4);
     A((void **)&t->units, ucap * sizeof(uint2));
     A((void **)&t->dctr, sizeof(Ctr));
+    A((void **)&t->des, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&t->hctr, sizeof(Ctr));
     if (e == cudaSuccess) e = cudaHostAlloc((void **)&t->mb, sizeof(Mailbox), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&t->dmb, t->mb, 0);
@@ -324,6 +340,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->q[1]);
     cudaFree(t->units);
     cudaFree(t->dctr);
+    cudaFree(t->des);
     if (t->hctr) cudaFreeHost(t->hctr);
     if (t->mb) cudaFreeHost(t->mb);
     for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
@@ -604,5 +621,40 @@ extern "C" int abfs_aggregate_count(int device, const int64_t *host_counts, size
     cudaFree(dt);
     if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("aggregate_count: ") + cudaGetErrorString(e));
     *total = (int64_t)h;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_traversal_instrument(abfs_traversal *t, int on) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    t->instrument = on != 0;
+    t->es_log.clear();
+    return ABFS_OK;
+}
+
+extern "C" int abfs_traversal_level_stats(abfs_traversal *t, size_t nlev, uint64_t *count,
+                                          uint64_t *out_deg, uint64_t *in_deg, uint64_t *scanned) {
+    if (!t || !count || !out_deg || !in_deg) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(t->device));
+    unsigned long long *h = nullptr;
+    const size_t cells = 3 * (nlev + 1);
+    ABFS_CUDA(cudaMalloc(&h, cells * sizeof(unsigned long long)));
+    cudaError_t e = cudaMemsetAsync(h, 0, cells * sizeof(unsigned long long), t->stream);
+    if (e == cudaSuccess) {
+        k_level_hist<<<148 * 8, kBlock, 0, t->stream>>>(t->depth, t->g->d.out_off, t->g->d.in_off,
+                                                       t->g->d.n, (uint32_t)nlev, h);
+        e = cudaGetLastError();
+    }
+    std::vector<unsigned long long> hv(cells);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), h, cells * 8, cudaMemcpyDeviceToHost, t->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(t->stream);
+    cudaFree(h);
+    if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("level_stats: ") + cudaGetErrorString(e));
+    for (size_t i = 0; i <= nlev; ++i) {
+        count[i] = hv[i];
+        out_deg[i] = hv[(nlev + 1) + i];
+        in_deg[i] = hv[2 * (nlev + 1) + i];
+    }
+    if (scanned)
+        for (size_t i = 0; i < nlev; ++i) scanned[i] = i < t->es_log.size() ? t->es_log[i] : 0;
     return ABFS_OK;
 }

@@ -202,6 +202,17 @@ class Traversal:
         L.check(L.lib().abfs_last_traversal_ns(self._h, ctypes.byref(v)), "last_ns")
         return v.value
 
+    def instrument(self, on: bool = True):
+        L.check(L.lib().abfs_traversal_instrument(self._h, int(on)), "instrument")
+
+    def level_stats(self, nlev: int):
+        """Per-depth (count, Σ out-degree, Σ in-degree) for depths < nlev plus
+        an unreached slot, and per-level pull-scanned edges (instrumented)."""
+        a = [np.zeros(nlev + 1, np.uint64) for _ in range(4)]
+        L.check(L.lib().abfs_traversal_level_stats(self._h, nlev, *[L.ptr(x, L.u64p) for x in a]),
+                "level_stats")
+        return {"count": a[0], "out_deg": a[1], "in_deg": a[2], "scanned": a[3][:nlev]}
+
     def reached(self):
         e, v = ctypes.c_uint64(), ctypes.c_uint64()
         L.check(L.lib().abfs_reached_edges(self._h, ctypes.byref(e), ctypes.byref(v)), "reached")
