@@ -202,6 +202,11 @@ class Traversal:
         L.check(L.lib().abfs_last_traversal_ns(self._h, ctypes.byref(v)), "last_ns")
         return v.value
 
+    def launches(self) -> int:
+        v = ctypes.c_uint64()
+        L.check(L.lib().abfs_traversal_launches(self._h, ctypes.byref(v)), "launches")
+        return v.value
+
     def instrument(self, on: bool = True):
         L.check(L.lib().abfs_traversal_instrument(self._h, int(on)), "instrument")
 
