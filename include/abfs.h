@@ -169,6 +169,11 @@ ABFS_API int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree 
  * from after init_depths to the final count readback. */
 ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
 
+/* 1 (default): bfs_full / adaptive_bfs run the whole level loop inside one
+ * persistent cooperative kernel (device-side FlatTree, grid barriers between
+ * levels); 0: one launch chain + one host round trip per level. */
+ABFS_API int abfs_traversal_set_mode(abfs_traversal *t, int device_loop);
+
 /* Number of kernels this traversal has launched (bench gpu_launches). */
 ABFS_API int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches);
 

@@ -45,6 +45,9 @@ struct Ctr {
     unsigned long long reached_vertices;
     unsigned int done;           // finished-CTA ticket of the publishing kernel
     unsigned int pad;
+    unsigned int cq3[3];         // megakernel: per-level compaction cursors
+    unsigned int pad2;
+    unsigned long long es3[3];   // megakernel: per-level pull scanned edges
 };
 
 // Host-mapped result of the last level (written by the device).
@@ -276,12 +279,10 @@ struct CEmit {
 // that sources[f] is gathered only when the claim could have an effect.
 // ---------------------------------------------------------------------------
 template <int VAR, bool REV>
-__global__ void __launch_bounds__(kBlock)
-k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
-       const uint32_t *__restrict__ gather_arr, uint64_t m) {
-    __shared__ SmemQ sq;
-    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
-    zero_slot(c);
+__device__ __forceinline__ void edge_body(const LevelCtx &c, SmemQ *sq,
+                                          const uint32_t *__restrict__ stream_arr,
+                                          const uint32_t *__restrict__ gather_arr, uint64_t m) {
+    QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     for (uint64_t tile = (uint64_t)blockIdx.x * kEdgeTile; tile < m;
          tile += (uint64_t)gridDim.x * kEdgeTile) {
@@ -348,6 +349,15 @@ k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
         em.tile_end();
     }
     em.finish();
+}
+
+template <int VAR, bool REV>
+__global__ void __launch_bounds__(kBlock)
+k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
+       const uint32_t *__restrict__ gather_arr, uint64_t m) {
+    __shared__ SmemQ sq;
+    zero_slot(c);
+    edge_body<VAR, REV>(c, &sq, stream_arr, gather_arr, m);
     publish(c);
 }
 
@@ -356,12 +366,11 @@ k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
 // one thread per frontier vertex walks its out-adjacency in order.
 // ---------------------------------------------------------------------------
 template <int VAR>
-__global__ void __launch_bounds__(kBlock)
-k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
-       const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
-    __shared__ SmemQ sq;
-    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
-    zero_slot(c);
+__device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
+                                          const uint32_t *__restrict__ q, uint32_t F,
+                                          const uint32_t *__restrict__ out_off,
+                                          const uint32_t *__restrict__ dst) {
+    QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     for (uint32_t base = blockIdx.x * kBlock; base < F; base += gridDim.x * kBlock) {
         const uint32_t i = base + threadIdx.x;
@@ -384,6 +393,15 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
         em.tile_end();
     }
     em.finish();
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
+       const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
+    __shared__ SmemQ sq;
+    zero_slot(c);
+    push_body<VAR>(c, &sq, q, F, out_off, dst);
     publish(c);
 }
 
@@ -394,18 +412,18 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
 // Vertices with degree > kHeavy are split into kUnit-edge CTA work units
 // processed by k_heavy (CTA-centric push), so hubs never serialise a warp.
 // ---------------------------------------------------------------------------
-template <int VAR, int VW>
-__global__ void __launch_bounds__(kBlock)
-k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
-            const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
-    __shared__ SmemQ sq;
-    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
-    zero_slot(c);
+template <int VAR>
+__device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
+                                               const uint32_t *__restrict__ q, uint32_t F,
+                                               const uint32_t *__restrict__ out_off,
+                                               const uint32_t *__restrict__ dst, int vw_log2) {
+    QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
-    constexpr uint32_t per = 32 / VW;               // frontier entries per warp step
-    constexpr uint32_t per_block = per * kWarps;
+    const uint32_t VW = 1u << vw_log2;
+    const uint32_t per = 32u >> vw_log2;            // frontier entries per warp step
+    const uint32_t per_block = per * kWarps;
     const unsigned lane = lane_id();
-    const uint32_t sub = lane / VW, sl = lane % VW;
+    const uint32_t sub = lane >> vw_log2, sl = lane & (VW - 1);
     const uint32_t wib = threadIdx.x >> 5;
     for (uint32_t bb = blockIdx.x * per_block; bb < F; bb += gridDim.x * per_block) {
         const uint32_t i = bb + wib * per + sub;
@@ -439,11 +457,20 @@ k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
     em.finish();
 }
 
-template <int VAR>
+template <int VAR, int VWL>
 __global__ void __launch_bounds__(kBlock)
-k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
+k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
+            const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
-    QEmit<VAR> em(&sq, c.q_next, c.q_tail);
+    zero_slot(c);
+    push_warp_body<VAR>(c, &sq, q, F, out_off, dst, VWL);
+}
+
+template <int VAR>
+__device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
+                                           const uint32_t *__restrict__ out_off,
+                                           const uint32_t *__restrict__ dst) {
+    QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     const unsigned nunits = *(volatile unsigned *)c.units_tail;
     for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
@@ -463,6 +490,13 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
         em.tile_end();
     }
     em.finish();
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
+    __shared__ SmemQ sq;
+    heavy_body<VAR>(c, &sq, out_off, dst);
     publish(c);
 }
 
@@ -480,13 +514,12 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // atomics, and every next-frontier word is written (no clearing pass).
 // ---------------------------------------------------------------------------
 template <int VAR>
-__global__ void __launch_bounds__(kBlock)
-k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
-       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t n,
-       uint64_t words) {
-    __shared__ unsigned int sn;
-    CEmit<VAR> em(&sn, c.count);
-    zero_slot(c);
+__device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
+                                          const uint32_t *__restrict__ in_off,
+                                          const uint32_t *__restrict__ src,
+                                          const uint32_t *__restrict__ noin,
+                                          uint32_t *__restrict__ fbm_next, uint64_t words) {
+    CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
@@ -581,13 +614,23 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
     }
 }
 
+template <int VAR>
+__global__ void __launch_bounds__(kBlock)
+k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
+       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t words) {
+    __shared__ unsigned int sn;
+    zero_slot(c);
+    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, words);
+}
+
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
 // segment of one vertex's in-list with early exit; the first unit to find a
 // frontier in-neighbour claims the vertex (atomicOr on its visited bit).
-__global__ void __launch_bounds__(kBlock)
-k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
-             uint32_t *fbm_next) {
-    __shared__ int s_done;
+__device__ __forceinline__ void pull_heavy_body(const LevelCtx &c, int *s_done_p,
+                                                const uint32_t *__restrict__ in_off,
+                                                const uint32_t *__restrict__ src,
+                                                uint32_t *fbm_next) {
+    int &s_done = *s_done_p;
     const unsigned nunits = *(volatile unsigned *)c.units_tail;
     for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
         const uint2 un = c.units[w];
@@ -621,6 +664,13 @@ k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__
         }
         __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
+             uint32_t *fbm_next) {
+    __shared__ int s_done;
+    pull_heavy_body(c, &s_done, in_off, src, fbm_next);
     publish(c);
 }
 
@@ -629,12 +679,12 @@ k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__
 // ---------------------------------------------------------------------------
 
 // bitmap -> queue: per-word popc, warp + CTA scan, one atomic per CTA.
-__global__ void __launch_bounds__(kBlock)
-k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
-                  unsigned int *cursor) {
-    __shared__ unsigned warp_tot[kWarps];
-    __shared__ unsigned base;
-    const uint64_t word = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+// One call covers the kBlock words starting at word0 (CTA-uniform).
+__device__ __forceinline__ void bitmap_to_queue_tile(const uint32_t *__restrict__ fbm,
+                                                     uint64_t words, uint64_t word0, uint32_t *q,
+                                                     unsigned int *cursor, unsigned *warp_tot,
+                                                     unsigned *base) {
+    const uint64_t word = word0 + threadIdx.x;
     uint32_t w = word < words ? fbm[word] : 0u;
     const unsigned cnt = __popc(w);
     const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
@@ -653,15 +703,24 @@ k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
             warp_tot[i] = acc;
             acc += t;
         }
-        base = acc ? atomicAdd(cursor, acc) : 0u;
+        *base = acc ? atomicAdd(cursor, acc) : 0u;
     }
     __syncthreads();
-    unsigned pos = base + warp_tot[wid] + incl - cnt;
+    unsigned pos = *base + warp_tot[wid] + incl - cnt;
+    __syncthreads();   // warp_tot / base are reused by the next tile
     while (w) {
         const int b = __ffs(w) - 1;
         q[pos++] = (uint32_t)(word * 32 + b);
         w &= w - 1;
     }
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
+                  unsigned int *cursor) {
+    __shared__ unsigned warp_tot[kWarps];
+    __shared__ unsigned base;
+    bitmap_to_queue_tile(fbm, words, (uint64_t)blockIdx.x * kBlock, q, cursor, warp_tot, &base);
 }
 
 // queue -> bitmap (bitmap cleared by the caller).

@@ -9,11 +9,12 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
 
-#include "bfs_kernels.cuh"
+#include "megakernel.cuh"
 
 namespace abfs {
 
@@ -59,6 +60,14 @@ struct abfs_traversal {
     unsigned long long *des = nullptr;   // pull scanned-edge counter (instrumented)
     bool instrument = false;
     std::vector<uint64_t> es_log;        // per level (instrumented runs)
+    // device-resident loop (megakernel)
+    bool use_mega = true;
+    MegaRecord *drecs = nullptr;
+    std::vector<MegaRecord> hrecs;
+    unsigned long long *dnlev = nullptr;
+    unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
+    size_t tree_cap = 0;
+    int mega_grid = 0;
 };
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
@@ -118,7 +127,7 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
         break;
     case ABFS_VERTEX_PULL:
         k_pull<VAR><<<grid_for(t->words, kBlock, 148 * 64), kBlock, 0, s>>>(
-            c, g.in_off, g.src, t->noin, t->fbm[t->cur ^ 1], g.n, t->words);
+            c, g.in_off, g.src, t->noin, t->fbm[t->cur ^ 1], t->words);
         k_pull_heavy<<<148 * 2, kBlock, 0, s>>>(c, g.in_off, g.src, t->fbm[t->cur ^ 1]);
         t->launches += 2;
         break;
@@ -127,12 +136,12 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
         const unsigned grid = grid_for((uint64_t)F * vw, kBlock, 148 * 32);
         const uint32_t *q = t->q[t->cur];
         switch (vw) {
-        case 32: k_push_warp<VAR, 32><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 16: k_push_warp<VAR, 16><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 8: k_push_warp<VAR, 8><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 4: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 2: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        default: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 32: k_push_warp<VAR, 5><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 16: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 8: k_push_warp<VAR, 3><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 4: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        case 2: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
+        default: k_push_warp<VAR, 0><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
         }
         k_heavy<VAR><<<148 * 2, kBlock, 0, s>>>(c, g.out_off, g.dst);
         t->launches += 2;
@@ -341,6 +350,10 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->units);
     cudaFree(t->dctr);
     cudaFree(t->des);
+    cudaFree(t->drecs);
+    cudaFree(t->dnlev);
+    cudaFree(t->dtree);
+    if (t->htree) cudaFreeHost(t->htree);
     if (t->hctr) cudaFreeHost(t->hctr);
     if (t->mb) cudaFreeHost(t->mb);
     for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
@@ -435,11 +448,152 @@ static int finish_traversal(abfs_traversal *t, size_t n_levels, int32_t *depths_
     return ABFS_OK;
 }
 
+constexpr uint32_t kMegaCap = 1u << 16;   // level records kept by the megakernel
+
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Run a whole traversal in the persistent cooperative kernel.  fixed_pair
+// >= 0 runs bfs_full with that pair; otherwise the tree picks per level.
+static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_tree *tr,
+                    const double *static24, int64_t chunk, size_t *n_levels) {
+    const DevGraph &g = t->g->d;
+    cudaStream_t s = t->stream;
+    ABFS_CUDA(cudaSetDevice(t->device));
+    if (!t->drecs) {
+        ABFS_CUDA(cudaMalloc(&t->drecs, kMegaCap * sizeof(MegaRecord)));
+        ABFS_CUDA(cudaMalloc(&t->dnlev, sizeof(unsigned long long)));
+    }
+    if (!t->mega_grid) {
+        int per = 0, sms = 0;
+        ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mega, kBlock, 0));
+        ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
+        if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
+        t->mega_grid = per * sms;
+    }
+    // stage tree + static features (small) into one device blob
+    const uint32_t nn = tr ? tr->node_count : 0, ns = tr ? tr->n_selection : 0;
+    const size_t o_sel = 0, o_feat = align16(o_sel + ns * 2), o_thr = align16(o_feat + nn * 2);
+    const size_t o_left = align16(o_thr + nn * 8), o_right = align16(o_left + nn * 4);
+    const size_t o_cls = align16(o_right + nn * 4), o_st = align16(o_cls + nn);
+    const size_t bytes = align16(o_st + 24 * 8);
+    if (bytes > t->tree_cap) {
+        cudaFree(t->dtree);
+        if (t->htree) cudaFreeHost(t->htree);
+        t->dtree = nullptr;
+        t->htree = nullptr;
+        ABFS_CUDA(cudaMalloc(&t->dtree, bytes * 2));
+        ABFS_CUDA(cudaMallocHost(&t->htree, bytes * 2));
+        t->tree_cap = bytes * 2;
+    }
+    ABFS_CUDA(cudaStreamSynchronize(s));   // staging blob may still be in flight
+    if (tr) {
+        std::memcpy(t->htree + o_sel, tr->selection, ns * 2);
+        std::memcpy(t->htree + o_feat, tr->features, nn * 2);
+        std::memcpy(t->htree + o_thr, tr->thresholds, nn * 8);
+        std::memcpy(t->htree + o_left, tr->lefts, nn * 4);
+        std::memcpy(t->htree + o_right, tr->rights, nn * 4);
+        std::memcpy(t->htree + o_cls, tr->leaf_classes, nn);
+    }
+    if (static24) std::memcpy(t->htree + o_st, static24, 24 * 8);
+    else std::memset(t->htree + o_st, 0, 24 * 8);
+    ABFS_CUDA(cudaMemcpyAsync(t->dtree, t->htree, bytes, cudaMemcpyHostToDevice, s));
+    ABFS_TRY(init_impl(t, root));
+    ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
+    ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3, s));
+    ABFS_TRY(ensure_events(t, 2));
+    MegaParams P;
+    P.depth = t->depth;
+    P.visited = t->visited;
+    P.noin = t->noin;
+    P.fbm0 = t->fbm[0];
+    P.fbm1 = t->fbm[1];
+    P.q0 = t->q[0];
+    P.q1 = t->q[1];
+    P.units = t->units;
+    P.ctr = t->dctr;
+    P.out_off = g.out_off;
+    P.dst = g.dst;
+    P.org = g.org;
+    P.in_off = g.in_off;
+    P.src = g.src;
+    P.rev_owner = g.rev_owner;
+    P.n = g.n;
+    P.m = g.m;
+    P.words = t->words;
+    P.sel = (const uint16_t *)(t->dtree + o_sel);
+    P.feat = (const uint16_t *)(t->dtree + o_feat);
+    P.thr = (const double *)(t->dtree + o_thr);
+    P.left = (const uint32_t *)(t->dtree + o_left);
+    P.right = (const uint32_t *)(t->dtree + o_right);
+    P.cls = (const uint8_t *)(t->dtree + o_cls);
+    P.static24 = (const double *)(t->dtree + o_st);
+    P.fixed_pair = fixed_pair;
+    P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
+    P.instrument = t->instrument ? 1 : 0;
+    P.cap = kMegaCap;
+    P.recs = t->drecs;
+    P.n_levels = t->dnlev;
+    ABFS_CUDA(cudaEventRecord(t->et0, s));
+    void *args[] = {&P};
+    ABFS_CUDA(cudaLaunchCooperativeKernel((void *)k_mega, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
+    t->launches += 1;
+    ABFS_CUDA(cudaEventRecord(t->ev[1], s));
+    unsigned long long nl = 0;
+    ABFS_CUDA(cudaMemcpyAsync(&nl, t->dnlev, sizeof(nl), cudaMemcpyDeviceToHost, s));
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    const size_t keep = nl < kMegaCap ? nl : kMegaCap;
+    t->hrecs.resize(keep);
+    if (keep)
+        ABFS_CUDA(cudaMemcpy(t->hrecs.data(), t->drecs, keep * sizeof(MegaRecord), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->ev[1]));
+    t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
+    // final state: depths + frontier of the terminating level are resident
+    const MegaRecord *last = keep ? &t->hrecs[keep - 1] : nullptr;
+    t->cur = (int)((nl - 1 + 1) & 1);
+    t->has_q = last && last->kernel != ABFS_VERTEX_PULL;
+    t->has_bm = !t->has_q;
+    t->F = 0;
+    t->expect_level = -1;
+    t->call = 0;
+    if (t->instrument) {
+        t->es_log.resize(keep);
+        for (size_t l = 0; l < keep; ++l) t->es_log[l] = t->hrecs[l].scanned;
+    }
+    *n_levels = (size_t)nl;
+    return ABFS_OK;
+}
+
+static uint64_t rec_ns(const MegaRecord &r) {
+    const uint64_t d = r.t_end > r.t_start ? r.t_end - r.t_start : 0;
+    return d ? d : 1;
+}
+
+extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    t->use_mega = device_loop != 0;
+    return ABFS_OK;
+}
+
 extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int variant,
                              int64_t chunk, int32_t *depths_out, uint64_t *counts,
                              uint64_t *elapsed, size_t cap, size_t *n_levels) {
     if (!t || !n_levels) return fail(ABFS_EINVAL, "null argument");
     ABFS_TRY(level_params_ok(0, kernel, variant, chunk));
+    if (t->use_mega) {
+        if (root < 0 || (uint64_t)root >= t->g->d.n)
+            return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
+                                         std::to_string(t->g->d.n));
+        size_t nl = 0;
+        ABFS_TRY(mega_run(t, root, kernel * 3 + variant, nullptr, nullptr, chunk, &nl));
+        *n_levels = nl;
+        for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
+            if (counts) counts[l] = t->hrecs[l].new_count;
+            if (elapsed) elapsed[l] = rec_ns(t->hrecs[l]);
+        }
+        if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
+        return ABFS_OK;
+    }
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
     size_t nl = 0;
@@ -527,6 +681,31 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
                                  abfs_level_record *recs, size_t cap, size_t *n_levels) {
     if (!t || !static24 || !n_levels) return fail(ABFS_EINVAL, "null argument");
     ABFS_TRY(tree_ok(tr));
+    if (t->use_mega) {
+        if (root < 0 || (uint64_t)root >= t->g->d.n)
+            return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
+                                         std::to_string(t->g->d.n));
+        size_t nl = 0;
+        ABFS_TRY(mega_run(t, root, -1, tr, static24, chunk, &nl));
+        *n_levels = nl;
+        if (recs)
+            for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
+                const MegaRecord &m = t->hrecs[l];
+                abfs_level_record &r = recs[l];
+                r.level = (int64_t)l;
+                r.kernel = m.kernel;
+                r.variant = m.variant;
+                r.fallback = m.fallback;
+                r.converted = m.converted;
+                r.frontier_size = m.frontier;
+                r.new_count = m.new_count;
+                r.elapsed_ns = rec_ns(m);
+                const uint64_t pn = m.t_pred > m.t_start ? m.t_pred - m.t_start : 0;
+                r.prediction_ns = pn ? pn : 1;
+            }
+        if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
+        return ABFS_OK;
+    }
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
     uint64_t frontier = 1, discovered = 1;

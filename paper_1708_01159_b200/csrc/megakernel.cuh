@@ -1,0 +1,224 @@
+// megakernel.cuh -- device-resident tree-switched level loop.
+//
+// One cooperative, persistent kernel runs the whole traversal: every CTA
+// evaluates the FlatTree on the reference's float64 features (identical
+// arithmetic, so all CTAs pick the same pair), runs the chosen strategy body
+// over the grid, and meets the others at a grid barrier; the new count is
+// read from the rotating counter slot after the barrier.  No host round trip
+// and no kernel launch between levels: the per-level fixed cost drops from a
+// launch + readback (~10 us) to one or two grid barriers.
+//
+// The strategy bodies are the same device functions the per-level kernels
+// use (bfs_kernels.cuh), so results are identical by construction; the
+// megakernel always starts from init_depths, hence runs in consistent mode.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "bfs_kernels.cuh"
+
+namespace abfs {
+
+namespace cg = cooperative_groups;
+
+struct MegaRecord {
+    int32_t kernel, variant, fallback, converted;
+    unsigned long long frontier, new_count;
+    unsigned long long t_start, t_pred, t_end;   // %globaltimer (ns)
+    unsigned long long scanned;                  // pull ES (instrumented)
+};
+
+struct MegaParams {
+    int32_t *depth;
+    uint32_t *visited;
+    const uint32_t *noin;
+    uint32_t *fbm0, *fbm1;
+    uint32_t *q0, *q1;
+    uint2 *units;
+    Ctr *ctr;
+    const uint32_t *out_off, *dst, *org, *in_off, *src, *rev_owner;
+    uint64_t n, m, words;
+    // tree (FlatTree arrays, device copies) and the 24 static features
+    const uint16_t *sel, *feat;
+    const double *thr;
+    const uint32_t *left, *right;
+    const uint8_t *cls;
+    const double *static24;
+    int fixed_pair;      // >= 0: bfs_full with this pair ordinal, no tree
+    int vw_log2;
+    int instrument;
+    uint32_t cap;
+    MegaRecord *recs;
+    unsigned long long *n_levels;
+};
+
+constexpr int kMegaMinBlocks = 3;   // register budget: <= 80 regs / thread
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int mega_tree_class(const MegaParams &P, unsigned long long frontier,
+                                               unsigned long long discovered) {
+    // extract_runtime_features (features.py:98-121) + FlatTree.predict_one
+    // (tree.py:332-339): float64 true division, strict < goes left.
+    const double nd = P.static24[0];
+    const unsigned long long nv = (unsigned long long)nd;
+    uint32_t node = 0;
+    while (P.cls[node] == 255) {
+        const int canon = P.sel[P.feat[node]];
+        double x;
+        switch (canon) {
+        case 2: x = (double)frontier; break;
+        case 3: x = (double)frontier / (double)nv; break;
+        case 4: x = (double)discovered; break;
+        case 5: x = (double)discovered / (double)nv; break;
+        default: x = P.static24[canon];
+        }
+        node = (x < P.thr[node]) ? P.left[node] : P.right[node];
+    }
+    return P.cls[node];
+}
+
+template <int VAR>
+__device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
+                                              uint32_t F, const uint32_t *q, uint32_t *fbm_next,
+                                              SmemQ *sq, unsigned *sn, int *s_done,
+                                              cg::grid_group &grid) {
+    switch (kernel) {
+    case 0:
+        edge_body<VAR, false>(c, sq, P.org, P.dst, P.m);
+        break;
+    case 1:
+        edge_body<VAR, true>(c, sq, P.rev_owner, P.src, P.m);
+        break;
+    case 2:
+        push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
+        break;
+    case 3:
+        pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, P.words);
+        grid.sync();
+        pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
+        break;
+    default:
+        push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2);
+        grid.sync();
+        heavy_body<VAR>(c, sq, P.out_off, P.dst);
+        break;
+    }
+    grid.sync();
+}
+
+__global__ void __launch_bounds__(kBlock, kMegaMinBlocks) k_mega(MegaParams P) {
+    __shared__ SmemQ sq;
+    __shared__ unsigned sn;
+    __shared__ int s_done;
+    __shared__ int s_cls;
+    __shared__ unsigned warp_tot[kWarps];
+    __shared__ unsigned s_base;
+    cg::grid_group grid = cg::this_grid();
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long frontier = 1, discovered = 1;
+    int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
+    int cur = 0;
+    bool has_q = true, has_bm = true;
+    for (uint32_t level = 0;; ++level) {
+        const unsigned long long t0 = lead ? globaltimer() : 0ull;
+        if (threadIdx.x == 0)
+            s_cls = P.fixed_pair >= 0 ? P.fixed_pair : mega_tree_class(P, frontier, discovered);
+        __syncthreads();
+        const int cls = s_cls;
+        const int fallback = cls == 254;
+        if (!fallback) {
+            pk = cls / 3;
+            pv = cls % 3;
+        }
+        const unsigned long long tp = lead ? globaltimer() : 0ull;
+        const int out = (int)(level % 3), zero = (int)((level + 1) % 3);
+        if (lead) {
+            P.ctr->qlen[zero] = 0;
+            P.ctr->units[zero] = 0;
+            P.ctr->count[zero] = 0;
+            P.ctr->cq3[zero] = 0;
+            P.ctr->es3[zero] = 0;
+        }
+        uint32_t *fbm_cur = cur ? P.fbm1 : P.fbm0, *fbm_nxt = cur ? P.fbm0 : P.fbm1;
+        uint32_t *q_cur = cur ? P.q1 : P.q0, *q_nxt = cur ? P.q0 : P.q1;
+        const bool need_queue = (pk == 2 || pk == 4);
+        int conv = 0;
+        if (need_queue && !has_q) {          // bitmap -> queue (switch cost)
+            for (uint64_t w0 = (uint64_t)blockIdx.x * kBlock; w0 < P.words;
+                 w0 += (uint64_t)gridDim.x * kBlock)
+                bitmap_to_queue_tile(fbm_cur, P.words, w0, q_cur, &P.ctr->cq3[out], warp_tot,
+                                     &s_base);
+            grid.sync();
+            has_q = true;
+            conv = 1;
+        } else if (!need_queue && !has_bm) { // queue -> bitmap (switch cost)
+            for (uint64_t w = (uint64_t)blockIdx.x * kBlock + threadIdx.x; w < P.words;
+                 w += (uint64_t)gridDim.x * kBlock)
+                fbm_cur[w] = 0u;
+            grid.sync();
+            for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < frontier;
+                 i += (uint64_t)gridDim.x * kBlock) {
+                const uint32_t v = q_cur[i];
+                atomicOr(fbm_cur + (v >> 5), 1u << (v & 31));
+            }
+            grid.sync();
+            has_bm = true;
+            conv = 1;
+        }
+        LevelCtx c;
+        c.depth = P.depth;
+        c.visited = P.visited;
+        c.fbm = fbm_cur;
+        c.q_next = q_nxt;
+        c.q_tail = &P.ctr->qlen[out];
+        c.count = &P.ctr->count[out];
+        c.units_tail = &P.ctr->units[out];
+        c.units = P.units;
+        c.inconsistent = &P.ctr->inconsistent;
+        c.ctr = P.ctr;
+        c.mb = nullptr;
+        c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
+        c.seq = 0;
+        c.zero_slot = zero;
+        c.level = (int32_t)level;
+        c.lvl1 = (int32_t)level + 1;
+        switch (pv) {
+        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
+        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
+        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
+        }
+        const bool topdown = pk != 3;
+        const unsigned long long nw = topdown
+            ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
+            : *(volatile unsigned long long *)&P.ctr->count[out];
+        if (lead && level < P.cap) {
+            MegaRecord &r = P.recs[level];
+            r.kernel = pk;
+            r.variant = pv;
+            r.fallback = fallback;
+            r.converted = conv;
+            r.frontier = frontier;
+            r.new_count = nw;
+            r.t_start = t0;
+            r.t_pred = tp;
+            r.t_end = globaltimer();
+            r.scanned = P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;
+        }
+        if (nw == 0) {
+            if (lead) *P.n_levels = (unsigned long long)level + 1;
+            return;
+        }
+        frontier = nw;
+        discovered += nw;
+        cur ^= 1;
+        has_q = topdown;
+        has_bm = !topdown;
+    }
+}
+
+}  // namespace abfs

@@ -202,6 +202,10 @@ class Traversal:
         L.check(L.lib().abfs_last_traversal_ns(self._h, ctypes.byref(v)), "last_ns")
         return v.value
 
+    def set_device_loop(self, on: bool):
+        """True (default): whole traversals run in the persistent megakernel."""
+        L.check(L.lib().abfs_traversal_set_mode(self._h, int(on)), "set_mode")
+
     def launches(self) -> int:
         v = ctypes.c_uint64()
         L.check(L.lib().abfs_traversal_launches(self._h, ctypes.byref(v)), "launches")
