@@ -194,3 +194,31 @@ def test_larger_random_graphs_vs_oracle():
                 np.array([n, m, 0, 0, 0, 0, *P.features.static_vector(stats)[6:]]))
             assert [(int(r.kernel), int(r.variant), r.fallback_used, r.frontier_size)
                     for r in tr.records] == [(k_, v_, fb, fr) for (_, k_, v_, fb, fr, *_x) in orecs]
+
+
+@pytest.mark.parametrize("name", ["kron12", "er12", "mesh64", "u1000", "path9", "star7"])
+def test_device_loop_and_launch_loop_agree(name):
+    """The persistent megakernel (default) and the per-level launch chain give
+    identical depths, counts and adaptive traces."""
+    g = graph(name)
+    t = g.device_graph().scratch()
+    flat = P.deserialize(G.tree_path("t1"))
+    stats = P.compute_stats(g)
+    try:
+        for r in G.roots(name):
+            res = {}
+            for loop in (True, False):
+                t.set_device_loop(loop)
+                pairs = []
+                for k, v in P.ALL_PAIRS:
+                    d, outs = P.bfs_full(g, r, k, v)
+                    pairs.append((d.copy(), [o.new_frontier_count for o in outs]))
+                d, tr = P.adaptive_bfs(g, r, flat, stats)
+                res[loop] = (pairs, d.copy(), tr.pairs, [x.frontier_size for x in tr.records])
+            for (d1, c1), (d2, c2) in zip(res[True][0], res[False][0]):
+                np.testing.assert_array_equal(d1, d2)
+                assert c1 == c2
+            np.testing.assert_array_equal(res[True][1], res[False][1])
+            assert res[True][2:] == res[False][2:]
+    finally:
+        t.set_device_loop(True)
