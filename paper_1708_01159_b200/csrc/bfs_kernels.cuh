@@ -80,8 +80,7 @@ struct LevelCtx {
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
-constexpr int kEdgeVec = 4;           // uint4 loads in flight per thread (edge stream)
-constexpr int kEdgeTile = kBlock * 4 * kEdgeVec;  // slots per CTA iteration
+constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 2048;     // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 4096;      // edges per CTA work unit
 constexpr uint32_t kPullLight = 32;   // pull: per-lane scan up to this in-degree
@@ -101,6 +100,7 @@ __device__ __forceinline__ void zero_slot(const LevelCtx &c) {
 // Last CTA to finish publishes (qlen, count) to the mapped mailbox.  Must be
 // reached by every thread of every CTA of the level's final kernel.
 __device__ __forceinline__ void publish(const LevelCtx &c) {
+    __threadfence();   // every thread's counter atomics are performed before the ticket
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -278,12 +278,13 @@ struct CEmit {
 // sources[f], tail rev_owner[f].  The sorted tail stream is read first so
 // that sources[f] is gathered only when the claim could have an effect.
 // ---------------------------------------------------------------------------
-template <int VAR, bool REV>
+template <int VAR, bool REV, int kEdgeVec = 4>
 __device__ __forceinline__ void edge_body(const LevelCtx &c, SmemQ *sq,
                                           const uint32_t *__restrict__ stream_arr,
                                           const uint32_t *__restrict__ gather_arr, uint64_t m) {
     QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
+    constexpr uint64_t kEdgeTile = kBlock * 4 * kEdgeVec;  // slots per CTA iteration
     for (uint64_t tile = (uint64_t)blockIdx.x * kEdgeTile; tile < m;
          tile += (uint64_t)gridDim.x * kEdgeTile) {
         uint4 t4[kEdgeVec];

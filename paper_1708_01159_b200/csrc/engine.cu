@@ -68,6 +68,7 @@ struct abfs_traversal {
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
     int mega_grid = 0;
+    int mega_minb = 6;
 };
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
@@ -112,12 +113,12 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
     const uint32_t F = (uint32_t)t->F;
     switch (kernel) {
     case ABFS_EDGE_LIST:
-        k_edge<VAR, false><<<grid_for(g.m, kEdgeTile, persist_grid(k_edge<VAR, false>)), kBlock, 0, s>>>(
+        k_edge<VAR, false><<<grid_for(g.m, kEdgeTileMax, persist_grid(k_edge<VAR, false>)), kBlock, 0, s>>>(
             c, g.org, g.dst, g.m);
         t->launches += 1;
         break;
     case ABFS_REV_EDGE_LIST:
-        k_edge<VAR, true><<<grid_for(g.m, kEdgeTile, persist_grid(k_edge<VAR, true>)), kBlock, 0, s>>>(
+        k_edge<VAR, true><<<grid_for(g.m, kEdgeTileMax, persist_grid(k_edge<VAR, true>)), kBlock, 0, s>>>(
             c, g.rev_owner, g.src, g.m);
         t->launches += 1;
         break;
@@ -463,9 +464,10 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
         ABFS_CUDA(cudaMalloc(&t->drecs, kMegaCap * sizeof(MegaRecord)));
         ABFS_CUDA(cudaMalloc(&t->dnlev, sizeof(unsigned long long)));
     }
+    void *kfn = t->mega_minb == 4 ? (void *)k_mega<4> : (void *)k_mega<6>;
     if (!t->mega_grid) {
         int per = 0, sms = 0;
-        ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mega, kBlock, 0));
+        ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
         ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
         if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
         t->mega_grid = per * sms;
@@ -535,7 +537,7 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     P.n_levels = t->dnlev;
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
-    ABFS_CUDA(cudaLaunchCooperativeKernel((void *)k_mega, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
+    ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
     t->launches += 1;
     ABFS_CUDA(cudaEventRecord(t->ev[1], s));
     unsigned long long nl = 0;
@@ -555,7 +557,8 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     t->has_bm = !t->has_q;
     t->F = 0;
     t->expect_level = -1;
-    t->call = 0;
+    t->call = 0;   // per-level path restarts its counter slots from zero
+    ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq) + sizeof(unsigned), s));
     if (t->instrument) {
         t->es_log.resize(keep);
         for (size_t l = 0; l < keep; ++l) t->es_log[l] = t->hrecs[l].scanned;
@@ -572,6 +575,11 @@ static uint64_t rec_ns(const MegaRecord &r) {
 extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
     t->use_mega = device_loop != 0;
+    const int minb = device_loop == 2 ? 4 : 6;
+    if (minb != t->mega_minb) {
+        t->mega_minb = minb;
+        t->mega_grid = 0;
+    }
     return ABFS_OK;
 }
 

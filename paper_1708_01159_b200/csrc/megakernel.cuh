@@ -52,7 +52,6 @@ struct MegaParams {
     unsigned long long *n_levels;
 };
 
-constexpr int kMegaMinBlocks = 3;   // register budget: <= 80 regs / thread
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -89,10 +88,10 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
                                               cg::grid_group &grid) {
     switch (kernel) {
     case 0:
-        edge_body<VAR, false>(c, sq, P.org, P.dst, P.m);
+        edge_body<VAR, false, 1>(c, sq, P.org, P.dst, P.m);
         break;
     case 1:
-        edge_body<VAR, true>(c, sq, P.rev_owner, P.src, P.m);
+        edge_body<VAR, true, 1>(c, sq, P.rev_owner, P.src, P.m);
         break;
     case 2:
         push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
@@ -111,7 +110,10 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
     grid.sync();
 }
 
-__global__ void __launch_bounds__(kBlock, kMegaMinBlocks) k_mega(MegaParams P) {
+// MINB = resident CTAs per SM the register budget is sized for (6 -> 40
+// registers, 4 -> 64); latency-bound pull levels want the higher occupancy.
+template <int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
     __shared__ unsigned sn;
     __shared__ int s_done;

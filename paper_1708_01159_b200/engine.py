@@ -202,8 +202,9 @@ class Traversal:
         L.check(L.lib().abfs_last_traversal_ns(self._h, ctypes.byref(v)), "last_ns")
         return v.value
 
-    def set_device_loop(self, on: bool):
-        """True (default): whole traversals run in the persistent megakernel."""
+    def set_device_loop(self, on):
+        """True/1 (default): whole traversals run in the persistent megakernel
+        (2: its 64-register variant); False/0: per-level launches."""
         L.check(L.lib().abfs_traversal_set_mode(self._h, int(on)), "set_mode")
 
     def launches(self) -> int:

@@ -67,7 +67,7 @@ def test_level_contract_and_inconsistent_inputs(name):
                 d = arr.copy()
                 out = P.run_level(g, d, level, k, v)
                 np.testing.assert_array_equal(d, want, err_msg=f"{name} L{level} k{k} v{v}")
-                assert out.new_frontier_count == cnt
+                assert out.new_frontier_count == cnt, (name, level, k, v)
             d64 = arr.astype(np.int64)
             P.run_level(g, d64, level, k, 0)
             np.testing.assert_array_equal(d64, want)

@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--out", default="gpurun_out/levels.csv")
     ap.add_argument("--stats", default="gpurun_out/stats.json")
+    ap.add_argument("--mode", type=int, default=1,
+                    help="1 megakernel (40 regs), 2 megakernel (64 regs), 0 per-level launches")
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     stats = {}
@@ -68,6 +70,7 @@ def main():
         if cfg.startswith("mesh"):
             roots = sorted(set([0, *roots]))
         t = Traversal(dg)
+        t.set_device_loop(a.mode)
         rows = benchmark_graph_gpu(dg, roots, cfg, a.reps, a.warmup, traversal=t)
         export_levels(rows, a.out, append=not first)
         first = False
