@@ -48,6 +48,7 @@ struct Ctr {
     unsigned int cq3[3];         // megakernel: per-level compaction cursors
     unsigned int pad2;
     unsigned long long es3[3];   // megakernel: per-level pull scanned edges
+    unsigned long long work[3];  // per-level dynamic work cursors
 };
 
 // Host-mapped result of the last level (written by the device).
@@ -71,6 +72,7 @@ struct LevelCtx {
     Ctr *ctr;
     Mailbox *mb;                 // device view of the host mailbox
     unsigned long long *es;      // optional: in-edges scanned by pull (instrumented runs)
+    unsigned long long *work;    // dynamic work cursor of this level (= &ctr->work[out])
     unsigned long long seq;
     int zero_slot;
     int32_t level;
@@ -93,6 +95,7 @@ __device__ __forceinline__ void zero_slot(const LevelCtx &c) {
         c.ctr->qlen[c.zero_slot] = 0;
         c.ctr->units[c.zero_slot] = 0;
         c.ctr->count[c.zero_slot] = 0;
+        c.ctr->work[c.zero_slot] = 0;
         c.ctr->cq = 0;
     }
 }
@@ -522,10 +525,15 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           uint32_t *__restrict__ fbm_next, uint64_t words) {
     CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
-    const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const uint64_t ntiles = (words + 31) / 32;
     unsigned long long scanned = 0;
-    for (uint64_t tile = warp; tile * 32 < words; tile += nwarps) {
+    for (;;) {
+        // dynamic tile fetch: one atomic per warp per 32-word tile
+        unsigned long long tile = 0;
+        if (lane == 0) tile = atomicAdd(c.work, 1ull);
+        tile = __shfl_sync(kFull, tile, 0);
+        if (tile >= ntiles) break;
         const uint64_t myw = tile * 32 + lane;
         uint32_t vis = 0xffffffffu, skip = 0xffffffffu;
         if (myw < words) {
@@ -547,56 +555,67 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 j = __ldg(in_off + v);
                 e = __ldg(in_off + v + 1);
             }
-            // phase A (every candidate): own list, 4 independent loads per
-            // step, at most kPullLight entries -- most vertices stop here
-            const uint32_t ja = min(e, j + kPullLight);
+            // phase A: each candidate probes its first 4 in-neighbours
+            // (independent loads) -- most vertices of a big level stop here
             bool found = false;
-            while (__any_sync(kFull, j < ja)) {
-                if (j < ja) {
-                    scanned += min(4u, ja - j);
-                    const uint32_t u0 = __ldg(src + j);
-                    const uint32_t u1 = j + 1 < ja ? __ldg(src + j + 1) : u0;
-                    const uint32_t u2 = j + 2 < ja ? __ldg(src + j + 2) : u0;
-                    const uint32_t u3 = j + 3 < ja ? __ldg(src + j + 3) : u0;
-                    if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
-                        in_bitmap(c.fbm, u3)) {
-                        found = true;
-                        j = e;
-                    } else {
-                        j = min(j + 4, ja);
-                    }
-                }
+            if (j < e) {
+                const uint32_t ja = min(e, j + 4);
+                scanned += ja - j;
+                const uint32_t u0 = __ldg(src + j);
+                const uint32_t u1 = j + 1 < ja ? __ldg(src + j + 1) : u0;
+                const uint32_t u2 = j + 2 < ja ? __ldg(src + j + 2) : u0;
+                const uint32_t u3 = j + 3 < ja ? __ldg(src + j + 3) : u0;
+                found = in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
+                        in_bitmap(c.fbm, u3);
+                j = found ? e : ja;
             }
-            // heavier lanes: cooperative warp scan, or CTA units
-            unsigned hm = __ballot_sync(kFull, cand && !found && j < e);
-            while (hm) {
-                const int l = __ffs(hm) - 1;
-                hm &= hm - 1;
-                const uint32_t hj = __shfl_sync(kFull, j, l), he = __shfl_sync(kFull, e, l);
-                if (he - hj > kPullHeavy) {
-                    if (lane == 0) {
-                        const uint32_t nu = (he - hj + kUnit - 1) / kUnit;
-                        const uint32_t s = atomicAdd(c.units_tail, nu);
-                        for (uint32_t k = 0; k < nu; ++k)
-                            c.units[s + k] = make_uint2((uint32_t)(word * 32 + l), k);
-                    }
-                    continue;
+            // super-heavy remainders go to CTA units (k_pull_heavy)
+            bool pend = !found && j < e;
+            if (pend && e - j > kPullHeavy) {
+                const uint32_t nu = (e - j + kUnit - 1) / kUnit;
+                const uint32_t s = atomicAdd(c.units_tail, nu);
+                for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2((uint32_t)v, k);
+                pend = false;
+            }
+            // phase B: the warp walks the concatenation of all pending
+            // remainders 128 entries per step (load-balanced, mostly
+            // coalesced), skipping owners already found, until every pending
+            // vertex has a frontier in-neighbour or the lists are exhausted
+            const unsigned pmask = __ballot_sync(kFull, pend);
+            if (pmask) {
+                const uint32_t rem = pend ? e - j : 0u;
+                uint32_t incl = rem;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= (unsigned)o) incl += t;
                 }
-                bool f = false;
-                for (uint32_t b = hj; b < he; b += 128) {
-                    scanned += (lane == 0) ? min(128u, he - b) : 0u;
-                    bool hit = false;
+                const uint32_t excl = incl - rem;
+                const uint32_t total = __shfl_sync(kFull, incl, 31);
+                unsigned fmask = 0;
+                for (uint32_t base = 0; base < total; base += 128) {
+                    unsigned hit_bits = 0;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const uint32_t x = b + k * 32 + lane;
-                        if (x < he) hit |= in_bitmap(c.fbm, __ldg(src + x));
+                        const uint32_t p = base + k * 32 + lane;
+                        // owner = last lane whose exclusive offset <= p
+                        int owner = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const uint32_t ex = __shfl_sync(kFull, excl, owner + step);
+                            if (ex <= p) owner += step;
+                        }
+                        const uint32_t oj = __shfl_sync(kFull, j, owner);
+                        const uint32_t oex = __shfl_sync(kFull, excl, owner);
+                        if (p < total && !((fmask >> owner) & 1u)) {
+                            ++scanned;
+                            if (in_bitmap(c.fbm, __ldg(src + oj + (p - oex)))) hit_bits |= 1u << owner;
+                        }
                     }
-                    if (__any_sync(kFull, hit)) {
-                        f = true;
-                        break;
-                    }
+                    fmask |= __reduce_or_sync(kFull, hit_bits);
+                    if ((fmask & pmask) == pmask) break;
                 }
-                if (lane == (unsigned)l) found = f;
+                found |= (fmask >> lane) & 1u;
             }
             const unsigned fm = __ballot_sync(kFull, found);
             if (found) c.depth[v] = c.lvl1;
@@ -607,6 +626,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             em.add(fm);
         }
     }
+    (void)lt_mask;
     em.finish();
     if (c.es) {
 #pragma unroll

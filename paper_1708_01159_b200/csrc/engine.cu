@@ -238,6 +238,7 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     c.ctr = t->dctr;
     c.mb = t->dmb;
     c.es = nullptr;
+    c.work = &t->dctr->work[out];
     if (t->instrument) {
         ABFS_CUDA(cudaMemsetAsync(t->des, 0, sizeof(unsigned long long), s));
         c.es = t->des;
@@ -501,7 +502,7 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     ABFS_CUDA(cudaMemcpyAsync(t->dtree, t->htree, bytes, cudaMemcpyHostToDevice, s));
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
-    ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3, s));
+    ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3 + 8 * 3, s));
     ABFS_TRY(ensure_events(t, 2));
     MegaParams P;
     P.depth = t->depth;
@@ -557,8 +558,10 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     t->has_bm = !t->has_q;
     t->F = 0;
     t->expect_level = -1;
-    t->call = 0;   // per-level path restarts its counter slots from zero
+    // the per-level path needs its counter slots zeroed again (all three, so
+    // any starting slot works; t->call keeps growing for mailbox stamps)
     ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq) + sizeof(unsigned), s));
+    ABFS_CUDA(cudaMemsetAsync(&t->dctr->work[0], 0, 8 * 3, s));
     if (t->instrument) {
         t->es_log.resize(keep);
         for (size_t l = 0; l < keep; ++l) t->es_log[l] = t->hrecs[l].scanned;

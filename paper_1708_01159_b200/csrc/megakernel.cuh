@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             P.ctr->count[zero] = 0;
             P.ctr->cq3[zero] = 0;
             P.ctr->es3[zero] = 0;
+            P.ctr->work[zero] = 0;
         }
         uint32_t *fbm_cur = cur ? P.fbm1 : P.fbm0, *fbm_nxt = cur ? P.fbm0 : P.fbm1;
         uint32_t *q_cur = cur ? P.q1 : P.q0, *q_nxt = cur ? P.q0 : P.q1;
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.ctr = P.ctr;
         c.mb = nullptr;
         c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
+        c.work = &P.ctr->work[out];
         c.seq = 0;
         c.zero_slot = zero;
         c.level = (int32_t)level;
