@@ -73,6 +73,7 @@ struct LevelCtx {
     Mailbox *mb;                 // device view of the host mailbox
     unsigned long long *es;      // optional: in-edges scanned by pull (instrumented runs)
     unsigned long long *work;    // dynamic work cursor of this level (= &ctr->work[out])
+    uint32_t pull_light;         // pull phase A: entries each lane scans alone
     unsigned long long seq;
     int zero_slot;
     int32_t level;
@@ -85,7 +86,7 @@ constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 2048;     // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 4096;      // edges per CTA work unit
-constexpr uint32_t kPullLight = 32;   // pull: per-lane scan up to this in-degree
+constexpr uint32_t kPullLight = 16;   // pull phase A default (ABFS_PULL_LIGHT overrides)
 constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -555,19 +556,26 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 j = __ldg(in_off + v);
                 e = __ldg(in_off + v + 1);
             }
-            // phase A: each candidate probes its first 4 in-neighbours
-            // (independent loads) -- most vertices of a big level stop here
+            // phase A: each candidate scans up to c.pull_light of its own
+            // in-neighbours, 4 independent loads per step (early exit)
             bool found = false;
-            if (j < e) {
-                const uint32_t ja = min(e, j + 4);
-                scanned += ja - j;
-                const uint32_t u0 = __ldg(src + j);
-                const uint32_t u1 = j + 1 < ja ? __ldg(src + j + 1) : u0;
-                const uint32_t u2 = j + 2 < ja ? __ldg(src + j + 2) : u0;
-                const uint32_t u3 = j + 3 < ja ? __ldg(src + j + 3) : u0;
-                found = in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
-                        in_bitmap(c.fbm, u3);
-                j = found ? e : ja;
+            const uint32_t ja = min(e, j + c.pull_light);
+            while (__any_sync(kFull, j < ja)) {
+                if (j < ja) {
+                    const uint32_t jb = min(ja, j + 4);
+                    scanned += jb - j;
+                    const uint32_t u0 = __ldg(src + j);
+                    const uint32_t u1 = j + 1 < jb ? __ldg(src + j + 1) : u0;
+                    const uint32_t u2 = j + 2 < jb ? __ldg(src + j + 2) : u0;
+                    const uint32_t u3 = j + 3 < jb ? __ldg(src + j + 3) : u0;
+                    if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
+                        in_bitmap(c.fbm, u3)) {
+                        found = true;
+                        j = e;
+                    } else {
+                        j = jb;
+                    }
+                }
             }
             // super-heavy remainders go to CTA units (k_pull_heavy)
             bool pend = !found && j < e;

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -83,6 +84,17 @@ static int level_params_ok(int64_t level, int kernel, int variant, int64_t chunk
     if (level < INT32_MIN || level > (int64_t)kInf - 2)
         return fail(ABFS_EINVAL, "level out of range");
     return ABFS_OK;
+}
+
+// Pull phase-A depth (tunable for experiments via ABFS_PULL_LIGHT).
+static uint32_t pull_light() {
+    static uint32_t v = 0;
+    if (!v) {
+        const char *e = getenv("ABFS_PULL_LIGHT");
+        v = e ? (uint32_t)atoi(e) : kPullLight;
+        if (v < 1) v = 1;
+    }
+    return v;
 }
 
 static inline unsigned grid_for(uint64_t items, uint64_t per_block, uint64_t cap) {
@@ -239,6 +251,7 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     c.mb = t->dmb;
     c.es = nullptr;
     c.work = &t->dctr->work[out];
+    c.pull_light = pull_light();
     if (t->instrument) {
         ABFS_CUDA(cudaMemsetAsync(t->des, 0, sizeof(unsigned long long), s));
         c.es = t->des;
@@ -523,16 +536,19 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     P.n = g.n;
     P.m = g.m;
     P.words = t->words;
-    P.sel = (const uint16_t *)(t->dtree + o_sel);
-    P.feat = (const uint16_t *)(t->dtree + o_feat);
-    P.thr = (const double *)(t->dtree + o_thr);
-    P.left = (const uint32_t *)(t->dtree + o_left);
-    P.right = (const uint32_t *)(t->dtree + o_right);
-    P.cls = (const uint8_t *)(t->dtree + o_cls);
-    P.static24 = (const double *)(t->dtree + o_st);
+    P.sel = (const uint16_t *)t->dtree;
+    P.tree_bytes = (uint32_t)bytes;
+    P.o_sel = (uint32_t)o_sel;
+    P.o_feat = (uint32_t)o_feat;
+    P.o_thr = (uint32_t)o_thr;
+    P.o_left = (uint32_t)o_left;
+    P.o_right = (uint32_t)o_right;
+    P.o_cls = (uint32_t)o_cls;
+    P.o_st = (uint32_t)o_st;
     P.fixed_pair = fixed_pair;
     P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
     P.instrument = t->instrument ? 1 : 0;
+    P.pull_light = pull_light();
     P.cap = kMegaCap;
     P.recs = t->drecs;
     P.n_levels = t->dnlev;

@@ -38,15 +38,14 @@ struct MegaParams {
     Ctr *ctr;
     const uint32_t *out_off, *dst, *org, *in_off, *src, *rev_owner;
     uint64_t n, m, words;
-    // tree (FlatTree arrays, device copies) and the 24 static features
-    const uint16_t *sel, *feat;
-    const double *thr;
-    const uint32_t *left, *right;
-    const uint8_t *cls;
-    const double *static24;
+    // tree blob (FlatTree arrays + the 24 static features), device copy;
+    // sel points at its start, o_* are byte offsets within it
+    const uint16_t *sel;
+    uint32_t tree_bytes, o_sel, o_feat, o_thr, o_left, o_right, o_cls, o_st;
     int fixed_pair;      // >= 0: bfs_full with this pair ordinal, no tree
     int vw_log2;
     int instrument;
+    uint32_t pull_light;
     uint32_t cap;
     MegaRecord *recs;
     unsigned long long *n_levels;
@@ -59,26 +58,38 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__device__ __forceinline__ int mega_tree_class(const MegaParams &P, unsigned long long frontier,
+// The FlatTree and the static features live in shared memory for the whole
+// traversal (grid barriers flush L1, so global reads would cost an L2 round
+// trip per node per level).
+constexpr uint32_t kMegaTreeSmem = 16384;   // bytes: trees up to ~800 nodes
+
+struct SmemTree {
+    const uint16_t *sel, *feat;
+    const double *thr, *st;
+    const uint32_t *left, *right;
+    const uint8_t *cls;
+};
+
+__device__ __forceinline__ int mega_tree_class(const SmemTree &T, unsigned long long frontier,
                                                unsigned long long discovered) {
     // extract_runtime_features (features.py:98-121) + FlatTree.predict_one
     // (tree.py:332-339): float64 true division, strict < goes left.
-    const double nd = P.static24[0];
+    const double nd = T.st[0];
     const unsigned long long nv = (unsigned long long)nd;
     uint32_t node = 0;
-    while (P.cls[node] == 255) {
-        const int canon = P.sel[P.feat[node]];
+    while (T.cls[node] == 255) {
+        const int canon = T.sel[T.feat[node]];
         double x;
         switch (canon) {
         case 2: x = (double)frontier; break;
         case 3: x = (double)frontier / (double)nv; break;
         case 4: x = (double)discovered; break;
         case 5: x = (double)discovered / (double)nv; break;
-        default: x = P.static24[canon];
+        default: x = T.st[canon];
         }
-        node = (x < P.thr[node]) ? P.left[node] : P.right[node];
+        node = (x < T.thr[node]) ? T.left[node] : T.right[node];
     }
-    return P.cls[node];
+    return T.cls[node];
 }
 
 template <int VAR>
@@ -120,8 +131,27 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ int s_cls;
     __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned s_base;
+    __shared__ __align__(16) unsigned char s_tree[kMegaTreeSmem];
     cg::grid_group grid = cg::this_grid();
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    // stage the tree blob (same layout as the device copy) into shared memory
+    SmemTree T;
+    {
+        const unsigned char *src_blob = reinterpret_cast<const unsigned char *>(P.sel);
+        const bool fits = P.tree_bytes <= kMegaTreeSmem;
+        const unsigned char *base = fits ? s_tree : src_blob;
+        if (fits)
+            for (uint32_t i = threadIdx.x * 16; i < P.tree_bytes; i += kBlock * 16)
+                *reinterpret_cast<uint4 *>(s_tree + i) = *reinterpret_cast<const uint4 *>(src_blob + i);
+        __syncthreads();
+        T.sel = reinterpret_cast<const uint16_t *>(base + P.o_sel);
+        T.feat = reinterpret_cast<const uint16_t *>(base + P.o_feat);
+        T.thr = reinterpret_cast<const double *>(base + P.o_thr);
+        T.left = reinterpret_cast<const uint32_t *>(base + P.o_left);
+        T.right = reinterpret_cast<const uint32_t *>(base + P.o_right);
+        T.cls = base + P.o_cls;
+        T.st = reinterpret_cast<const double *>(base + P.o_st);
+    }
     unsigned long long frontier = 1, discovered = 1;
     int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
     int cur = 0;
@@ -129,7 +159,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     for (uint32_t level = 0;; ++level) {
         const unsigned long long t0 = lead ? globaltimer() : 0ull;
         if (threadIdx.x == 0)
-            s_cls = P.fixed_pair >= 0 ? P.fixed_pair : mega_tree_class(P, frontier, discovered);
+            s_cls = P.fixed_pair >= 0 ? P.fixed_pair : mega_tree_class(T, frontier, discovered);
         __syncthreads();
         const int cls = s_cls;
         const int fallback = cls == 254;
@@ -187,6 +217,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.mb = nullptr;
         c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
         c.work = &P.ctr->work[out];
+        c.pull_light = P.pull_light;
         c.seq = 0;
         c.zero_slot = zero;
         c.level = (int32_t)level;
