@@ -86,7 +86,7 @@ constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 2048;     // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 4096;      // edges per CTA work unit
-constexpr uint32_t kPullLight = 16;   // pull phase A default (ABFS_PULL_LIGHT overrides)
+constexpr uint32_t kPullLight = 32;   // pull phase A default (ABFS_PULL_LIGHT overrides)
 constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

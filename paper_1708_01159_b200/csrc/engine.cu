@@ -478,7 +478,7 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
         ABFS_CUDA(cudaMalloc(&t->drecs, kMegaCap * sizeof(MegaRecord)));
         ABFS_CUDA(cudaMalloc(&t->dnlev, sizeof(unsigned long long)));
     }
-    void *kfn = t->mega_minb == 4 ? (void *)k_mega<4> : (void *)k_mega<6>;
+    void *kfn = t->mega_minb == 5 ? (void *)k_mega<5> : (void *)k_mega<6>;
     if (!t->mega_grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -594,7 +594,7 @@ static uint64_t rec_ns(const MegaRecord &r) {
 extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
     t->use_mega = device_loop != 0;
-    const int minb = device_loop == 2 ? 4 : 6;
+    const int minb = device_loop == 2 ? 5 : 6;
     if (minb != t->mega_minb) {
         t->mega_minb = minb;
         t->mega_grid = 0;
