@@ -184,6 +184,7 @@ def run_ours(a):
     flat = P.deserialize(a.model)
     tree = flat.as_abfs()
     trav = Traversal(dg)
+    trav.set_device_loop(a.mode)
     stream = torch.cuda.Stream(device=dev)
     trav.set_stream(stream.cuda_stream)
 
@@ -308,6 +309,7 @@ def run_ours(a):
             "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
                        "scale": a.scale, "vertices": V, "directed_edge_slots": E,
                        "roots_per_step": R, "roots_pool": 64,
+                       "level_loop": "device (persistent megakernel)" if a.mode else "host (per-level launches)",
                        "model": os.path.relpath(a.model, ROOT),
                        "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
                        "l2": "inputs larger than L2 (graph arrays 8.1 GB)"},
@@ -421,6 +423,8 @@ def main():
     ap.add_argument("--model", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--mode", type=int, default=1,
+                    help="1: device-resident level loop (megakernel); 0: per-level launches")
     a = ap.parse_args()
     a.model = os.path.abspath(a.model) if a.model else default_model()
     if a.warmup < 3:

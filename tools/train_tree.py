@@ -32,56 +32,93 @@ def stats_from_vec(v):
     return ab.GraphStats(int(v[0]), int(v[1]), s[0], s[1], s[2])
 
 
+def quantize(samples, q):
+    """Round level times to a geometric grid of ratio (1+q): variants whose
+    times differ by less than the GPU's run-to-run noise then tie, and the
+    reference's label_level breaks the tie toward the lowest ordinal, which
+    gives consistent labels for similar levels (the trainer is unchanged)."""
+    import dataclasses
+    import math
+    if q <= 0:
+        return samples
+    out = []
+    for s_ in samples:
+        b = lambda t: float((1 + q) ** round(math.log(max(t, 1.0)) / math.log(1 + q)))
+        out.append(dataclasses.replace(s_, mean_ns=b(s_.mean_ns), min_ns=int(b(s_.min_ns))))
+    return out
+
+
+def replay(flat, training, table):
+    """Σ over runs of the measured cost of the tree's per-level choices."""
+    by_run = {}
+    for t in training:
+        by_run.setdefault((t.graph_id, t.root), []).append(t)
+    cost = {}
+    for key in sorted(by_run):
+        prev, c_ = 0, 0
+        for t in sorted(by_run[key], key=lambda t: t.level):
+            c = flat.predict_one(t.features)
+            c = prev if c == 254 else c
+            prev = c
+            c_ += table[(key[0], key[1], t.level, c)]
+        cost[key] = c_
+    return cost
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--levels", required=True)
     ap.add_argument("--stats", required=True)
     ap.add_argument("--out", required=True)
-    ap.add_argument("--max-depth", type=int, default=8)
-    ap.add_argument("--min-leaf", type=int, default=2)
-    ap.add_argument("--min-split", type=int, default=4)
     ap.add_argument("--metric", default="min")
+    ap.add_argument("--max-levels", type=int, default=64)
+    ap.add_argument("--grid", default="0,0.03,0.06,0.1/4,6,8,12/1,2,4",
+                    help="quantisations / max depths / min leaf sizes to search")
     a = ap.parse_args()
-    samples = ab.read_samples(a.levels)
+    raw = ab.read_samples(a.levels)
     with open(a.stats) as fh:
         stats_map = {k: stats_from_vec(v) for k, v in json.load(fh).items()}
-    training = ab.training_samples_from(samples, stats_map, metric=a.metric)
-    cfg = ab.TrainConfig(max_depth=a.max_depth, min_samples_leaf=a.min_leaf,
-                         min_samples_split=a.min_split)
-    x, y = ab.to_matrix(training, ab.DEFAULT_MODEL_FEATURES)
-    tree = ab.fit(x, y, ab.DEFAULT_MODEL_FEATURES, cfg)
-    flat = ab.flatten(tree)
-    rep = ab.evaluate(flat, x, y)
-    print(f"samples={len(training)} nodes={flat.node_count} train_acc={rep.top1_accuracy:.3f} "
-          f"unknown={rep.unknown_rate:.3f}")
-    if len(training) >= 10:
-        tr, te = ab.split_train_test(training, 0.7, seed=0)
-        xt, yt = ab.to_matrix(tr, ab.DEFAULT_MODEL_FEATURES)
-        xe, ye = ab.to_matrix(te, ab.DEFAULT_MODEL_FEATURES)
-        held = ab.evaluate(ab.fit(xt, yt, ab.DEFAULT_MODEL_FEATURES, cfg), xe, ye)
-        print(f"held-out top1={held.top1_accuracy:.3f} (70/30 split)")
+    # measured table and the feature vector of every level of every run
+    table = {(s_.graph_id, s_.root, s_.level, ab.pair_index(s_.kernel, s_.variant)): s_.min_ns
+             for s_ in raw}
+    all_levels = ab.training_samples_from(raw, stats_map, metric=a.metric)
+    opt = {}
+    for t in all_levels:
+        best = min(table[(t.graph_id, t.root, t.level, i)] for i in range(15))
+        opt[(t.graph_id, t.root)] = opt.get((t.graph_id, t.root), 0) + best
+    depth = {}
+    for s_ in raw:
+        depth[(s_.graph_id, s_.root)] = max(depth.get((s_.graph_id, s_.root), 0), s_.level + 1)
+    sub = [s_ for s_ in raw if depth[(s_.graph_id, s_.root)] <= a.max_levels
+           or s_.level % (depth[(s_.graph_id, s_.root)] // a.max_levels + 1) == 0]
+    qs, depths, leaves = (list(map(float if i == 0 else int, g.split(",")))
+                          for i, g in enumerate(a.grid.split("/")))
+    best = None
+    for q in qs:
+        training = ab.training_samples_from(quantize(sub, q), stats_map, metric=a.metric)
+        x, y = ab.to_matrix(training, ab.DEFAULT_MODEL_FEATURES)
+        for d in depths:
+            for leaf in leaves:
+                cfg = ab.TrainConfig(max_depth=d, min_samples_leaf=leaf,
+                                     min_samples_split=max(2, 2 * leaf))
+                flat = ab.flatten(ab.fit(x, y, ab.DEFAULT_MODEL_FEATURES, cfg))
+                cost = replay(flat, all_levels, table)
+                score = float(np.exp(np.mean([np.log(cost[k] / opt[k]) for k in cost])))
+                worst = max(cost[k] / opt[k] for k in cost)
+                print(f"q={q:<5} depth={d:<3} leaf={leaf}: nodes={flat.node_count:4d} "
+                      f"geomean tree/opt={score:.4f} worst={worst:.3f}", flush=True)
+                if best is None or (score, worst) < best[0]:
+                    best = ((score, worst), q, d, leaf, flat, cost)
+    (score, worst), q, d, leaf, flat, cost = best
     ab.serialize(flat, a.out)
-    # replay: cost of the tree's per-level choice from the measured table
-    table = {}
-    for s in samples:
-        table[(s.graph_id, s.root, s.level, ab.pair_index(s.kernel, s.variant))] = s.min_ns
-    opt = ab.compute_optimal(samples)
-    orc = ab.compute_oracle(samples)
-    by_run = {}
-    for t in training:
-        by_run.setdefault((t.graph_id, t.root), []).append(t)
-    for key in sorted(by_run):
-        prev = 0
-        cost = 0
-        for t in sorted(by_run[key], key=lambda t: t.level):
-            c = flat.predict_one(t.features)
-            c = prev if c == 254 else c
-            prev = c
-            cost += table[(key[0], key[1], t.level, c)]
+    print(f"\nchosen: q={q} max_depth={d} min_leaf={leaf} nodes={flat.node_count} "
+          f"geomean tree/opt={score:.4f} worst={worst:.3f} -> {a.out}")
+    orc = ab.compute_oracle(raw)
+    for key in sorted(cost):
         k, v, o = orc[key]
         print(f"{key[0]:10s} root={key[1]:9d} optimal={opt[key]/1e3:9.1f}us "
-              f"best_single={o/1e3:9.1f}us ({k.name}/{v.name}) tree={cost/1e3:9.1f}us "
-              f"tree/opt={cost/opt[key]:.3f} single/tree={o/cost:.2f}")
+              f"best_single={o/1e3:9.1f}us ({k.name}/{v.name}) tree={cost[key]/1e3:9.1f}us "
+              f"tree/opt={cost[key]/opt[key]:.3f} single/tree={o/cost[key]:.2f}")
 
 
 if __name__ == "__main__":
