@@ -51,6 +51,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="k20,k22,k24")
     ap.add_argument("--roots", type=int, default=4)
+    ap.add_argument("--root-seed", type=int, default=1)
+    ap.add_argument("--mesh-roots", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--out", default="gpurun_out/levels.csv")
@@ -66,7 +68,8 @@ def main():
         dg = make(cfg)
         st = P.compute_stats(dg)
         stats[cfg] = static_vector(st).tolist()
-        roots = pick_roots(dg, a.roots if not cfg.startswith("mesh") else max(1, a.roots // 2))
+        roots = pick_roots(dg, a.roots if not cfg.startswith("mesh") else a.mesh_roots,
+                           seed=a.root_seed)
         if cfg.startswith("mesh"):
             roots = sorted(set([0, *roots]))
         t = Traversal(dg)
