@@ -7,6 +7,7 @@
 // Host decides the next (kernel, variant) from the reference's float64
 // features and the FlatTree (adaptive.py:101-129).
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
@@ -70,6 +71,8 @@ struct abfs_traversal {
     size_t tree_cap = 0;
     int mega_grid = 0;
     int mega_minb = 6;
+    char *stage = nullptr;                     // pinned D2H staging (2 chunks)
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
@@ -369,6 +372,9 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->dnlev);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
+    if (t->stage) cudaFreeHost(t->stage);
+    for (cudaEvent_t e : t->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (t->hctr) cudaFreeHost(t->hctr);
     if (t->mb) cudaFreeHost(t->mb);
     for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
@@ -429,12 +435,47 @@ extern "C" int abfs_load_depths(abfs_traversal *t, const int32_t *host) {
     return ABFS_OK;
 }
 
+// Depths to a caller (pageable) buffer: large arrays go through two pinned
+// staging chunks, the D2H of chunk k+1 overlapping the multi-threaded host
+// copy of chunk k (pageable cudaMemcpy alone is several times slower).
+constexpr size_t kStageChunk = 8u << 20;   // bytes
+
 extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
     if (!t || !host) return fail(ABFS_EINVAL, "null argument");
     ABFS_CUDA(cudaSetDevice(t->device));
-    ABFS_CUDA(cudaMemcpyAsync(host, t->depth, t->g->d.n * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost, t->stream));
-    ABFS_CUDA(cudaStreamSynchronize(t->stream));
+    const size_t bytes = t->g->d.n * sizeof(int32_t);
+    if (bytes < 2 * kStageChunk) {
+        ABFS_CUDA(cudaMemcpyAsync(host, t->depth, bytes, cudaMemcpyDeviceToHost, t->stream));
+        ABFS_CUDA(cudaStreamSynchronize(t->stream));
+        return ABFS_OK;
+    }
+    if (!t->stage) {
+        ABFS_CUDA(cudaMallocHost(&t->stage, 2 * kStageChunk));
+        for (int i = 0; i < 2; ++i) ABFS_CUDA(cudaEventCreateWithFlags(&t->stage_ev[i], cudaEventDisableTiming));
+    }
+    const char *dsrc = reinterpret_cast<const char *>(t->depth);
+    char *dst = reinterpret_cast<char *>(host);
+    const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+    auto issue = [&](size_t k) -> cudaError_t {
+        const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+        cudaError_t e = cudaMemcpyAsync(t->stage + (k & 1) * kStageChunk, dsrc + off, len,
+                                        cudaMemcpyDeviceToHost, t->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(t->stage_ev[k & 1], t->stream);
+        return e;
+    };
+    ABFS_CUDA(issue(0));
+    for (size_t k = 0; k < nchunks; ++k) {
+        if (k + 1 < nchunks) ABFS_CUDA(issue(k + 1));
+        ABFS_CUDA(cudaEventSynchronize(t->stage_ev[k & 1]));
+        const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+        const char *from = t->stage + (k & 1) * kStageChunk;
+        const int parts = 8;
+#pragma omp parallel for num_threads(parts) schedule(static)
+        for (int p = 0; p < parts; ++p) {
+            const size_t a = len * p / parts, b = len * (p + 1) / parts;
+            std::memcpy(dst + off + a, from + a, b - a);
+        }
+    }
     return ABFS_OK;
 }
 
@@ -495,6 +536,9 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     if (bytes > t->tree_cap) {
         cudaFree(t->dtree);
         if (t->htree) cudaFreeHost(t->htree);
+    if (t->stage) cudaFreeHost(t->stage);
+    for (cudaEvent_t e : t->stage_ev)
+        if (e) cudaEventDestroy(e);
         t->dtree = nullptr;
         t->htree = nullptr;
         ABFS_CUDA(cudaMalloc(&t->dtree, bytes * 2));

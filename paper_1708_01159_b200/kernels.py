@@ -86,9 +86,29 @@ def worker_count() -> int:
     return _worker_count
 
 
+_foreign_uploads: dict = {}
+
+
 def _device(graph):
-    """DeviceGraph for a host Graph (cached upload) or a DeviceGraph."""
-    return graph.device_graph() if hasattr(graph, "device_graph") else graph
+    """DeviceGraph for a host Graph (cached upload), a DeviceGraph, or any
+    object with the reference Graph's fields (e.g. an adaptive_bfs.Graph),
+    uploaded once and cached for the object's lifetime."""
+    if hasattr(graph, "device_graph"):
+        return graph.device_graph()
+    if hasattr(graph, "out_offsets") and hasattr(graph, "sources"):
+        key = id(graph)
+        dg = _foreign_uploads.get(key)
+        if dg is None:
+            import weakref
+            from .engine import DeviceGraph
+            dg = DeviceGraph.upload(graph)
+            _foreign_uploads[key] = dg
+            try:
+                weakref.finalize(graph, _foreign_uploads.pop, key, None)
+            except TypeError:
+                pass
+        return dg
+    return graph
 
 
 def _check_root(graph, root: int) -> None:
