@@ -153,30 +153,6 @@ __device__ __forceinline__ bool claim(const LevelCtx &c, uint32_t v, bool consis
     return true;
 }
 
-// Warp-cooperative claim (all 32 lanes call it together).  Lanes whose
-// candidates share a visited word merge their bits into ONE atomicOr (hub
-// adjacency lists and sorted reverse slots hit the same words repeatedly);
-// among lanes holding the same vertex (duplicate edges) only the lowest may
-// win, so each INF -> level+1 transition is still counted exactly once.
-__device__ __forceinline__ bool claim_warp(const LevelCtx &c, bool valid, uint32_t v,
-                                           bool consistent) {
-    if (!consistent) return valid && claim(c, v, false);
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t word = v >> 5, bit = 1u << (v & 31);
-    const bool pre = valid && !((c.visited[word] >> (v & 31)) & 1u);
-    const unsigned long long solo = 0x100000000ull | lane;
-    const unsigned peers = __match_any_sync(kFull, pre ? (unsigned long long)word : solo);
-    const unsigned same_v = __match_any_sync(kFull, pre ? (unsigned long long)v : solo);
-    const unsigned gbits = __reduce_or_sync(peers, pre ? bit : 0u);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (pre && lane == (unsigned)leader) old = atomicOr(c.visited + word, gbits);
-    old = __shfl_sync(peers, old, leader);
-    const bool won = pre && (__ffs(same_v) - 1 == (int)lane) && !(old & bit);
-    if (won) c.depth[v] = c.lvl1;
-    return won;
-}
-
 // ---------------------------------------------------------------------------
 // Count epilogues (aggregate_count kernels.py:143-170).
 // QEmit: winners append to the next queue; the append cursor IS the count.
@@ -360,18 +336,17 @@ __device__ __forceinline__ void edge_body(const LevelCtx &c, SmemQ *sq,
                 const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    bool cand = false;
+                    bool won = false;
                     uint32_t v = 0;
                     if (act[h][k]) {
                         if (!REV) {
                             v = __ldg(gather_arr + e + k);
-                            cand = true;
+                            won = claim(c, v, consistent);
                         } else {
                             v = s4[k];
-                            cand = in_bitmap(c.fbm, __ldg(gather_arr + e + k));
+                            if (in_bitmap(c.fbm, __ldg(gather_arr + e + k))) won = claim(c, v, consistent);
                         }
                     }
-                    const bool won = claim_warp(c, cand, v, consistent);
                     em.emit(won, v);
                 }
             }
@@ -411,13 +386,13 @@ __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
             e = __ldg(out_off + u + 1);
         }
         while (__any_sync(kFull, j < e)) {
-            const bool valid = j < e;
+            bool won = false;
             uint32_t v = 0;
-            if (valid) {
+            if (j < e) {
                 v = __ldg(dst + j);
                 ++j;
+                won = claim(c, v, consistent);
             }
-            const bool won = claim_warp(c, valid, v, consistent);
             em.emit(won, v);
         }
         em.tile_end();
@@ -473,13 +448,13 @@ __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
             }
         }
         while (__any_sync(kFull, j < e)) {
-            const bool valid = j < e;
+            bool won = false;
             uint32_t v = 0;
-            if (valid) {
+            if (j < e) {
                 v = __ldg(dst + j);
                 j += VW;
+                won = claim(c, v, consistent);
             }
-            const bool won = claim_warp(c, valid, v, consistent);
             em.emit(won, v);
         }
         em.tile_end();
@@ -509,9 +484,12 @@ __device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
         const uint32_t e = min(__ldg(out_off + un.x + 1), b + kUnit);
         for (uint32_t jb = b; jb < e; jb += kBlock) {
             const uint32_t j = jb + threadIdx.x;
-            const bool valid = j < e;
-            const uint32_t v = valid ? __ldg(dst + j) : 0u;
-            const bool won = claim_warp(c, valid, v, consistent);
+            bool won = false;
+            uint32_t v = 0;
+            if (j < e) {
+                v = __ldg(dst + j);
+                won = claim(c, v, consistent);
+            }
             em.emit(won, v);
         }
         em.tile_end();
