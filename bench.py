@@ -260,7 +260,8 @@ def run_ours(a):
     if os.path.exists(tf):
         try:
             with open(tf) as fh:
-                traffic = json.load(fh).get(KERNEL_NAMES[dom])
+                tr = json.load(fh).get(KERNEL_NAMES[dom])
+                traffic = round(tr["bytes_per_launch_mean"]) if tr else None
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -269,6 +270,7 @@ def run_ours(a):
                 "kernel_share_of_step": round(dom_ns / total_ns, 3),
                 "launches_measured": per_kernel[dom][2],
                 "algorithmic_bytes": int(dom_bytes),
+                "algorithmic_bytes_per_launch": int(dom_bytes / max(1, per_kernel[dom][2])),
                 "whole_traversal_GBps": round(sum(v[1] for v in per_kernel.values()) /
                                               (total_ns * 1e-9) / 1e9, 1)}
 

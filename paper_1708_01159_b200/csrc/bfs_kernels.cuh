@@ -84,8 +84,8 @@ constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
-constexpr uint32_t kHeavy = 2048;     // push-warp: degree above -> CTA units
-constexpr uint32_t kUnit = 4096;      // edges per CTA work unit
+constexpr uint32_t kHeavy = 256;      // push-warp: degree above -> CTA units
+constexpr uint32_t kUnit = 1024;      // edges per CTA work unit (4 steps of 256)
 constexpr uint32_t kPullLight = 32;   // pull phase A default (ABFS_PULL_LIGHT overrides)
 constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
 

@@ -144,7 +144,7 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
     case ABFS_VERTEX_PULL:
         k_pull<VAR><<<grid_for(t->words, kBlock, 148 * 64), kBlock, 0, s>>>(
             c, g.in_off, g.src, t->noin, t->fbm[t->cur ^ 1], t->words);
-        k_pull_heavy<<<148 * 2, kBlock, 0, s>>>(c, g.in_off, g.src, t->fbm[t->cur ^ 1]);
+        k_pull_heavy<<<148 * 8, kBlock, 0, s>>>(c, g.in_off, g.src, t->fbm[t->cur ^ 1]);
         t->launches += 2;
         break;
     default: {  // VERTEX_PUSH_WARP: nearest legal virtual-warp width <= chunk
@@ -159,7 +159,7 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
         case 2: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
         default: k_push_warp<VAR, 0><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
         }
-        k_heavy<VAR><<<148 * 2, kBlock, 0, s>>>(c, g.out_off, g.dst);
+        k_heavy<VAR><<<148 * 8, kBlock, 0, s>>>(c, g.out_off, g.dst);
         t->launches += 2;
     }
     }
@@ -317,7 +317,7 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     t->words = (n + 31) / 32;
     const uint64_t wpad = t->words + 4;
     const uint64_t qcap = n + 4;
-    const uint64_t ucap = m / 2048 + 64;   // units of both heavy paths
+    const uint64_t ucap = m / kHeavy + 64;   // units of both heavy paths (<= deg/kHeavy each)
     cudaError_t e = cudaSuccess;
     auto A = [&](void **p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
