@@ -192,6 +192,11 @@ ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *ve
 
 /* ---- helpers ------------------------------------------------------------ */
 
+/* Page-lock caller memory so depth read-backs into it are direct DMA (the
+ * Python layer's recycled output arrays; no reference counterpart). */
+ABFS_API int abfs_host_register(void *ptr, size_t bytes);
+ABFS_API int abfs_host_unregister(void *ptr);
+
 /* aggregate_count (kernels.py:143-170) on the device with the three
  * reduction shapes: DIRECT = 1 atomic/item, GROUP = warp reduce + 1
  * atomic/warp, TWO_LEVEL = warp + CTA reduce + 1 atomic/CTA. */

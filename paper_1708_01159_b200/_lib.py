@@ -87,6 +87,8 @@ _SIGNATURES = {
     "abfs_tree_predict": (ctypes.c_int, [ctypes.POINTER(AbfsTree), f64p,
                                          ctypes.POINTER(ctypes.c_int)]),
     "abfs_features": (ctypes.c_int, [f64p, ctypes.c_uint64, ctypes.c_uint64, f64p]),
+    "abfs_host_register": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
+    "abfs_host_unregister": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 _lib = None

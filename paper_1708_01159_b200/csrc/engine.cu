@@ -64,9 +64,11 @@ struct abfs_traversal {
     std::vector<uint64_t> es_log;        // per level (instrumented runs)
     // device-resident loop (megakernel)
     bool use_mega = true;
-    MegaRecord *drecs = nullptr;
+    MegaRecord *mrecs = nullptr;         // host-mapped level records (written by the kernel)
+    MegaRecord *drecs = nullptr;         // device view of mrecs
     std::vector<MegaRecord> hrecs;
-    unsigned long long *dnlev = nullptr;
+    unsigned long long *mnlev = nullptr, *dnlev = nullptr;   // host-mapped level count
+    std::vector<unsigned char> last_blob;                    // tree blob resident on the device
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
     int mega_grid = 0;
@@ -368,8 +370,8 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->units);
     cudaFree(t->dctr);
     cudaFree(t->des);
-    cudaFree(t->drecs);
-    cudaFree(t->dnlev);
+    if (t->mrecs) cudaFreeHost(t->mrecs);
+    if (t->mnlev) cudaFreeHost(t->mnlev);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
     if (t->stage) cudaFreeHost(t->stage);
@@ -444,7 +446,11 @@ extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
     if (!t || !host) return fail(ABFS_EINVAL, "null argument");
     ABFS_CUDA(cudaSetDevice(t->device));
     const size_t bytes = t->g->d.n * sizeof(int32_t);
-    if (bytes < 2 * kStageChunk) {
+    cudaPointerAttributes pa;
+    const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    if (!pinned) cudaGetLastError();   // clear a sticky-free lookup error
+    if (pinned || bytes < 2 * kStageChunk) {
         ABFS_CUDA(cudaMemcpyAsync(host, t->depth, bytes, cudaMemcpyDeviceToHost, t->stream));
         ABFS_CUDA(cudaStreamSynchronize(t->stream));
         return ABFS_OK;
@@ -515,9 +521,13 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     const DevGraph &g = t->g->d;
     cudaStream_t s = t->stream;
     ABFS_CUDA(cudaSetDevice(t->device));
-    if (!t->drecs) {
-        ABFS_CUDA(cudaMalloc(&t->drecs, kMegaCap * sizeof(MegaRecord)));
-        ABFS_CUDA(cudaMalloc(&t->dnlev, sizeof(unsigned long long)));
+    if (!t->mrecs) {
+        // level records go straight to host-mapped memory (one 64-byte posted
+        // write per level), so a traversal needs a single stream sync
+        ABFS_CUDA(cudaHostAlloc((void **)&t->mrecs, kMegaCap * sizeof(MegaRecord), cudaHostAllocMapped));
+        ABFS_CUDA(cudaHostGetDevicePointer((void **)&t->drecs, t->mrecs, 0));
+        ABFS_CUDA(cudaHostAlloc((void **)&t->mnlev, sizeof(unsigned long long), cudaHostAllocMapped));
+        ABFS_CUDA(cudaHostGetDevicePointer((void **)&t->dnlev, t->mnlev, 0));
     }
     void *kfn = t->mega_minb == 5 ? (void *)k_mega<5> : (void *)k_mega<6>;
     if (!t->mega_grid) {
@@ -536,27 +546,30 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     if (bytes > t->tree_cap) {
         cudaFree(t->dtree);
         if (t->htree) cudaFreeHost(t->htree);
-    if (t->stage) cudaFreeHost(t->stage);
-    for (cudaEvent_t e : t->stage_ev)
-        if (e) cudaEventDestroy(e);
         t->dtree = nullptr;
         t->htree = nullptr;
+        t->last_blob.clear();
         ABFS_CUDA(cudaMalloc(&t->dtree, bytes * 2));
         ABFS_CUDA(cudaMallocHost(&t->htree, bytes * 2));
         t->tree_cap = bytes * 2;
     }
-    ABFS_CUDA(cudaStreamSynchronize(s));   // staging blob may still be in flight
+    std::vector<unsigned char> blob(bytes, 0);
     if (tr) {
-        std::memcpy(t->htree + o_sel, tr->selection, ns * 2);
-        std::memcpy(t->htree + o_feat, tr->features, nn * 2);
-        std::memcpy(t->htree + o_thr, tr->thresholds, nn * 8);
-        std::memcpy(t->htree + o_left, tr->lefts, nn * 4);
-        std::memcpy(t->htree + o_right, tr->rights, nn * 4);
-        std::memcpy(t->htree + o_cls, tr->leaf_classes, nn);
+        std::memcpy(blob.data() + o_sel, tr->selection, ns * 2);
+        std::memcpy(blob.data() + o_feat, tr->features, nn * 2);
+        std::memcpy(blob.data() + o_thr, tr->thresholds, nn * 8);
+        std::memcpy(blob.data() + o_left, tr->lefts, nn * 4);
+        std::memcpy(blob.data() + o_right, tr->rights, nn * 4);
+        std::memcpy(blob.data() + o_cls, tr->leaf_classes, nn);
     }
-    if (static24) std::memcpy(t->htree + o_st, static24, 24 * 8);
-    else std::memset(t->htree + o_st, 0, 24 * 8);
-    ABFS_CUDA(cudaMemcpyAsync(t->dtree, t->htree, bytes, cudaMemcpyHostToDevice, s));
+    if (static24) std::memcpy(blob.data() + o_st, static24, 24 * 8);
+    if (blob != t->last_blob) {
+        // every mega_run ends with a stream sync, so the pinned staging copy
+        // is never in flight here; an unchanged tree is not re-uploaded
+        std::memcpy(t->htree, blob.data(), bytes);
+        ABFS_CUDA(cudaMemcpyAsync(t->dtree, t->htree, bytes, cudaMemcpyHostToDevice, s));
+        t->last_blob.swap(blob);
+    }
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
     ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3 + 8 * 3, s));
@@ -596,18 +609,16 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     P.cap = kMegaCap;
     P.recs = t->drecs;
     P.n_levels = t->dnlev;
+    *(volatile unsigned long long *)t->mnlev = 0;
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
     ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
     t->launches += 1;
     ABFS_CUDA(cudaEventRecord(t->ev[1], s));
-    unsigned long long nl = 0;
-    ABFS_CUDA(cudaMemcpyAsync(&nl, t->dnlev, sizeof(nl), cudaMemcpyDeviceToHost, s));
     ABFS_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long nl = *(volatile unsigned long long *)t->mnlev;
     const size_t keep = nl < kMegaCap ? nl : kMegaCap;
-    t->hrecs.resize(keep);
-    if (keep)
-        ABFS_CUDA(cudaMemcpy(t->hrecs.data(), t->drecs, keep * sizeof(MegaRecord), cudaMemcpyDeviceToHost));
+    t->hrecs.assign(t->mrecs, t->mrecs + keep);
     float ms = 0.f;
     ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->ev[1]));
     t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
@@ -906,5 +917,17 @@ extern "C" int abfs_traversal_level_stats(abfs_traversal *t, size_t nlev, uint64
     }
     if (scanned)
         for (size_t i = 0; i < nlev; ++i) scanned[i] = i < t->es_log.size() ? t->es_log[i] : 0;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_host_register(void *ptr, size_t bytes) {
+    if (!ptr || !bytes) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_host_unregister(void *ptr) {
+    if (!ptr) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaHostUnregister(ptr));
     return ABFS_OK;
 }

@@ -175,8 +175,7 @@ class Traversal:
 
     def bfs_full(self, root: int, kernel: int, variant: int, chunk_size: int = 32,
                  depths_out: np.ndarray | None = None, cap: int = 1 << 20):
-        counts = np.zeros(cap, np.uint64)
-        el = np.zeros(cap, np.uint64)
+        counts, el = self._level_arrays(cap)
         nl = ctypes.c_size_t()
         L.check(L.lib().abfs_bfs_full(self._h, int(root), int(kernel), int(variant),
                                       int(chunk_size),
@@ -184,18 +183,34 @@ class Traversal:
                                       L.ptr(counts, L.u64p), L.ptr(el, L.u64p), cap,
                                       ctypes.byref(nl)), "bfs_full")
         k = min(nl.value, cap)
-        return counts[:k], el[:k]
+        return counts[:k].copy(), el[:k].copy()
 
     def adaptive(self, root: int, tree: L.AbfsTree, static24: np.ndarray, chunk_size: int = 32,
                  depths_out: np.ndarray | None = None, cap: int = 1 << 16):
-        recs = (L.AbfsLevelRecord * cap)()
+        recs = self._records(cap)
         nl = ctypes.c_size_t()
         st = np.ascontiguousarray(static24, dtype=np.float64)
         L.check(L.lib().abfs_adaptive_bfs(
             self._h, int(root), ctypes.byref(tree), L.ptr(st, L.f64p), int(chunk_size),
             L.ptr(depths_out, L.i32p) if depths_out is not None else None, recs, cap,
             ctypes.byref(nl)), "adaptive_bfs")
-        return recs[:min(nl.value, cap)]
+        return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:min(nl.value, cap)]]
+
+    def _records(self, cap: int):
+        # one record buffer per traversal (allocating 3.6 MB per call would
+        # dominate short traversals)
+        buf = getattr(self, "_recbuf", None)
+        if buf is None or len(buf) < cap:
+            buf = (L.AbfsLevelRecord * cap)()
+            self._recbuf = buf
+        return buf
+
+    def _level_arrays(self, cap: int):
+        arr = getattr(self, "_lvlbuf", None)
+        if arr is None or arr[0].size < cap:
+            arr = (np.empty(cap, np.uint64), np.empty(cap, np.uint64))
+            self._lvlbuf = arr
+        return arr
 
     def last_ns(self) -> int:
         v = ctypes.c_uint64()

@@ -27,6 +27,7 @@ from enum import IntEnum
 
 import numpy as np
 
+from .hostmem import depth_array
 from . import _lib as L
 
 INF_DEPTH = np.iinfo(np.int32).max
@@ -122,7 +123,7 @@ def init_depths(graph, root: int) -> np.ndarray:
     _check_root(graph, root)
     t = _device(graph).scratch()
     t.init(root)
-    return t.read()
+    return t.read(depth_array(graph.vertex_count))
 
 
 def aggregate_count(local_counts, variant: CountVariant) -> int:
@@ -201,7 +202,7 @@ def bfs_full(graph, root: int, kernel: KernelId, variant: CountVariant,
     _check_root(graph, root)
     k, v = _validate(kernel, variant, chunk_size)
     t = _device(graph).scratch()
-    depths = np.empty(graph.vertex_count, dtype=DEPTH_DTYPE)
+    depths = depth_array(graph.vertex_count)
     counts, elapsed = t.bfs_full(root, k, v, chunk_size, depths_out=depths,
                                  cap=min(graph.vertex_count + 2, 1 << 20))
     return depths, [LevelOutcome(int(c), int(e)) for c, e in zip(counts, elapsed)]
