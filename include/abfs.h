@@ -190,6 +190,44 @@ ABFS_API int abfs_traversal_level_stats(abfs_traversal *t, size_t nlev, uint64_t
 /* Sum over reached vertices of out-degree (GTEPS numerator basis). */
 ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices);
 
+/* ---- 1-D vertex partition ---------------------------------- */
+
+/* One rank's share of a vertex-partitioned BFS: the destination range
+ * [lo, hi) (lo a multiple of 32; hi a multiple of 32 or |V|) of graph g,
+ * i.e. the destination-filtered out-CSR over all sources plus the owned
+ * in-CSR rows, owned depths/visited bits and a replicated global frontier
+ * bitmap.  There is no reference counterpart (the reference is one process,
+ * kernels.py:82-127); the per-level semantics are run_level's
+ * (kernels.py:340-353) restricted to owned destinations. */
+typedef struct abfs_part abfs_part;
+ABFS_API int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part **out);
+ABFS_API void abfs_part_destroy(abfs_part *p);
+ABFS_API int abfs_part_info(const abfs_part *p, uint64_t *lo, uint64_t *hi, uint64_t *m_fwd,
+                            uint64_t *m_rev);
+ABFS_API int abfs_part_set_stream(abfs_part *p, void *cuda_stream);
+/* init_depths (kernels.py:134-140) on the owned slice; frontier = {root}. */
+ABFS_API int abfs_part_init(abfs_part *p, int64_t root);
+/* One level on the local slice; writes this rank's next-frontier bitmap
+ * slice into the DEVICE buffer send[0..stride) (zero padded).  Enqueued on
+ * the partition's stream, no host sync: the caller all-gathers `send`
+ * (rank-major, stride words each) on the same stream, then calls
+ * abfs_part_exchange. */
+ABFS_API int abfs_part_level(abfs_part *p, int64_t level, int kernel, int variant,
+                             int64_t chunk_size, uint32_t *send, uint64_t stride);
+/* Unpack the gathered slices (DEVICE, nranks x stride words; word_bounds =
+ * host array of nranks+1 global word offsets) into the global frontier;
+ * global_count = popc of it (identical on every rank), local_count = this
+ * rank's count through the level's count variant, elapsed_ns = device time
+ * from the level's start to here (exchange included).  One host sync. */
+ABFS_API int abfs_part_exchange(abfs_part *p, const uint32_t *gathered,
+                                const uint64_t *word_bounds, uint32_t nranks, uint64_t stride,
+                                uint64_t *global_count, uint64_t *local_count,
+                                uint64_t *elapsed_ns);
+/* Owned depths (hi - lo entries) to host / to a device buffer (async). */
+ABFS_API int abfs_part_read_depths(abfs_part *p, int32_t *host_owned);
+ABFS_API int abfs_part_depths_device(abfs_part *p, int32_t *dev_out);
+ABFS_API int abfs_part_launches(const abfs_part *p, uint64_t *launches);
+
 /* ---- helpers ------------------------------------------------------------ */
 
 /* Page-lock caller memory so depth read-backs into it are direct DMA (the

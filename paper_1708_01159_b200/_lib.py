@@ -87,6 +87,18 @@ _SIGNATURES = {
     "abfs_tree_predict": (ctypes.c_int, [ctypes.POINTER(AbfsTree), f64p,
                                          ctypes.POINTER(ctypes.c_int)]),
     "abfs_features": (ctypes.c_int, [f64p, ctypes.c_uint64, ctypes.c_uint64, f64p]),
+    "abfs_part_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, vpp]),
+    "abfs_part_destroy": (None, [ctypes.c_void_p]),
+    "abfs_part_info": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p, u64p, u64p]),
+    "abfs_part_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "abfs_part_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
+    "abfs_part_level": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64]),
+    "abfs_part_exchange": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, u64p, ctypes.c_uint32,
+                                          ctypes.c_uint64, u64p, u64p, u64p]),
+    "abfs_part_read_depths": (ctypes.c_int, [ctypes.c_void_p, i32p]),
+    "abfs_part_depths_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "abfs_part_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),
     "abfs_host_register": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
     "abfs_host_unregister": (ctypes.c_int, [ctypes.c_void_p]),
 }

@@ -523,11 +523,14 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ in_off,
                                           const uint32_t *__restrict__ src,
                                           const uint32_t *__restrict__ noin,
-                                          uint32_t *__restrict__ fbm_next, uint64_t words) {
+                                          uint32_t *__restrict__ fbm_next, uint64_t word0,
+                                          uint64_t words) {
+    // words [word0, words) of the bitmaps (a vertex partition passes its
+    // owned range; bitmap/offset pointers are indexed by global ids)
     CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
     const unsigned lt_mask = (1u << lane) - 1u;
-    const uint64_t ntiles = (words + 31) / 32;
+    const uint64_t ntiles = (words - word0 + 31) / 32;
     unsigned long long scanned = 0;
     for (;;) {
         // dynamic tile fetch: one atomic per warp per 32-word tile
@@ -535,7 +538,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
         if (lane == 0) tile = atomicAdd(c.work, 1ull);
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= ntiles) break;
-        const uint64_t myw = tile * 32 + lane;
+        const uint64_t myw = word0 + tile * 32 + lane;
         uint32_t vis = 0xffffffffu, skip = 0xffffffffu;
         if (myw < words) {
             vis = c.visited[myw];
@@ -546,7 +549,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
         while (need) {
             const int wl = __ffs(need) - 1;
             need &= need - 1;
-            const uint64_t word = tile * 32 + wl;
+            const uint64_t word = word0 + tile * 32 + wl;
             const uint32_t wvis = __shfl_sync(kFull, vis, wl);
             const uint32_t wskip = __shfl_sync(kFull, skip, wl);
             const uint64_t v = word * 32 + lane;
@@ -646,10 +649,11 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
-       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t words) {
+       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t word0,
+       uint64_t words) {
     __shared__ unsigned int sn;
     zero_slot(c);
-    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, words);
+    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, word0, words);
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
@@ -695,7 +699,7 @@ __device__ __forceinline__ void pull_heavy_body(const LevelCtx &c, int *s_done_p
     }
 }
 
-__global__ void __launch_bounds__(kBlock)
+static __global__ void __launch_bounds__(kBlock)
 k_pull_heavy(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
              uint32_t *fbm_next) {
     __shared__ int s_done;
@@ -744,7 +748,7 @@ __device__ __forceinline__ void bitmap_to_queue_tile(const uint32_t *__restrict_
     }
 }
 
-__global__ void __launch_bounds__(kBlock)
+static __global__ void __launch_bounds__(kBlock)
 k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
                   unsigned int *cursor) {
     __shared__ unsigned warp_tot[kWarps];
@@ -753,7 +757,7 @@ k_bitmap_to_queue(const uint32_t *__restrict__ fbm, uint64_t words, uint32_t *q,
 }
 
 // queue -> bitmap (bitmap cleared by the caller).
-__global__ void k_queue_to_bitmap(const uint32_t *__restrict__ q, uint32_t F, uint32_t *fbm) {
+static __global__ void k_queue_to_bitmap(const uint32_t *__restrict__ q, uint32_t F, uint32_t *fbm) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
         const uint32_t v = q[i];
         atomicOr(fbm + (v >> 5), 1u << (v & 31));
@@ -761,7 +765,7 @@ __global__ void k_queue_to_bitmap(const uint32_t *__restrict__ q, uint32_t F, ui
 }
 
 // init_depths (kernels.py:134-140) + frontier {root} in both forms.
-__global__ void k_init(int32_t *depth, uint32_t *visited, uint32_t *fbm, uint32_t *q,
+static __global__ void k_init(int32_t *depth, uint32_t *visited, uint32_t *fbm, uint32_t *q,
                        uint64_t n, uint64_t words, uint32_t root) {
     const uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (word >= words) return;
@@ -785,7 +789,7 @@ __global__ void k_init(int32_t *depth, uint32_t *visited, uint32_t *fbm, uint32_
 }
 
 // noin: bit v set iff in-degree(v) == 0 or v >= n (padding).
-__global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, uint64_t words,
+static __global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, uint64_t words,
                        uint32_t *noin) {
     const uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (word >= words) return;
@@ -798,7 +802,7 @@ __global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, uint64_t
 }
 
 // Rebuild frontier bitmap + visited bitmap from an arbitrary depth array.
-__global__ void __launch_bounds__(kBlock)
+static __global__ void __launch_bounds__(kBlock)
 k_prepare(const int32_t *__restrict__ depth, uint64_t n, uint64_t words, int32_t level,
           uint32_t *fbm, uint32_t *visited, Ctr *ctr) {
     const unsigned lane = lane_id();
@@ -821,7 +825,7 @@ k_prepare(const int32_t *__restrict__ depth, uint64_t n, uint64_t words, int32_t
 }
 
 // Σ out-degree over reached vertices (GTEPS numerator) + reached count.
-__global__ void __launch_bounds__(kBlock)
+static __global__ void __launch_bounds__(kBlock)
 k_reached(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_off,
           uint64_t n, Ctr *ctr) {
     unsigned long long e = 0, r = 0;
@@ -845,7 +849,7 @@ k_reached(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_of
 
 // Per-depth histograms for the work model (bench roofline): for each depth
 // d < nlev: vertex count, Σ out-degree, Σ in-degree; slot nlev = unreached.
-__global__ void __launch_bounds__(kBlock)
+static __global__ void __launch_bounds__(kBlock)
 k_level_hist(const int32_t *__restrict__ depth, const uint32_t *__restrict__ out_off,
              const uint32_t *__restrict__ in_off, uint64_t n, uint32_t nlev,
              unsigned long long *hist /* 3 * (nlev + 1) */) {

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "launch.cuh"
 #include "megakernel.cuh"
 
 namespace abfs {
@@ -80,17 +81,6 @@ struct abfs_traversal {
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
 extern "C" int abfs_version(void) { return 1; }
 
-static int level_params_ok(int64_t level, int kernel, int variant, int64_t chunk) {
-    if (kernel < 0 || kernel > 4) return fail(ABFS_EINVAL, "unknown kernel " + std::to_string(kernel));
-    if (variant < 0 || variant > 2)
-        return fail(ABFS_EINVAL, "unknown count variant " + std::to_string(variant));
-    if (kernel == ABFS_VERTEX_PUSH_WARP && chunk < 1)
-        return fail(ABFS_EINVAL, "chunk_size must be >= 1");
-    if (level < INT32_MIN || level > (int64_t)kInf - 2)
-        return fail(ABFS_EINVAL, "level out of range");
-    return ABFS_OK;
-}
-
 // Pull phase-A depth (tunable for experiments via ABFS_PULL_LIGHT).
 static uint32_t pull_light() {
     static uint32_t v = 0;
@@ -102,69 +92,26 @@ static uint32_t pull_light() {
     return v;
 }
 
-static inline unsigned grid_for(uint64_t items, uint64_t per_block, uint64_t cap) {
-    uint64_t b = (items + per_block - 1) / per_block;
-    if (b < 1) b = 1;
-    if (b > cap) b = cap;
-    return (unsigned)b;
-}
-
-// One full wave of resident CTAs for a persistent kernel (cached per kernel).
-template <typename K>
-static uint64_t persist_grid(K kernel) {
-    static uint64_t grid = 0;
-    if (!grid) {
-        int dev = 0, sms = 148, per = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kBlock, 0);
-        grid = (uint64_t)sms * (uint64_t)(per > 0 ? per : 1);
-    }
-    return grid;
-}
-
+// One level's strategy launch over a StratArgs view (launch.cuh).
 template <int VAR>
 static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, int64_t chunk) {
     const DevGraph &g = t->g->d;
-    cudaStream_t s = t->stream;
-    const uint32_t F = (uint32_t)t->F;
-    switch (kernel) {
-    case ABFS_EDGE_LIST:
-        k_edge<VAR, false><<<grid_for(g.m, kEdgeTileMax, persist_grid(k_edge<VAR, false>)), kBlock, 0, s>>>(
-            c, g.org, g.dst, g.m);
-        t->launches += 1;
-        break;
-    case ABFS_REV_EDGE_LIST:
-        k_edge<VAR, true><<<grid_for(g.m, kEdgeTileMax, persist_grid(k_edge<VAR, true>)), kBlock, 0, s>>>(
-            c, g.rev_owner, g.src, g.m);
-        t->launches += 1;
-        break;
-    case ABFS_VERTEX_PUSH:
-        k_push<VAR><<<grid_for(F, kBlock, 148 * 64), kBlock, 0, s>>>(c, t->q[t->cur], F, g.out_off, g.dst);
-        t->launches += 1;
-        break;
-    case ABFS_VERTEX_PULL:
-        k_pull<VAR><<<grid_for(t->words, kBlock, 148 * 64), kBlock, 0, s>>>(
-            c, g.in_off, g.src, t->noin, t->fbm[t->cur ^ 1], t->words);
-        k_pull_heavy<<<148 * 8, kBlock, 0, s>>>(c, g.in_off, g.src, t->fbm[t->cur ^ 1]);
-        t->launches += 2;
-        break;
-    default: {  // VERTEX_PUSH_WARP: nearest legal virtual-warp width <= chunk
-        const int vw = chunk >= 32 ? 32 : chunk >= 16 ? 16 : chunk >= 8 ? 8 : chunk >= 4 ? 4 : chunk >= 2 ? 2 : 1;
-        const unsigned grid = grid_for((uint64_t)F * vw, kBlock, 148 * 32);
-        const uint32_t *q = t->q[t->cur];
-        switch (vw) {
-        case 32: k_push_warp<VAR, 5><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 16: k_push_warp<VAR, 4><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 8: k_push_warp<VAR, 3><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 4: k_push_warp<VAR, 2><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        case 2: k_push_warp<VAR, 1><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        default: k_push_warp<VAR, 0><<<grid, kBlock, 0, s>>>(c, q, F, g.out_off, g.dst); break;
-        }
-        k_heavy<VAR><<<148 * 8, kBlock, 0, s>>>(c, g.out_off, g.dst);
-        t->launches += 2;
-    }
-    }
+    StratArgs a;
+    a.out_off = g.out_off;
+    a.dst = g.dst;
+    a.org = g.org;
+    a.m_fwd = g.m;
+    a.in_off = g.in_off;
+    a.src = g.src;
+    a.rev_owner = g.rev_owner;
+    a.m_rev = g.m;
+    a.noin = t->noin;
+    a.fbm_next = t->fbm[t->cur ^ 1];
+    a.word0 = 0;
+    a.word_end = t->words;
+    a.q = t->q[t->cur];
+    a.F = (uint32_t)t->F;
+    t->launches += launch_strategy_args<VAR>(c, a, kernel, chunk, t->stream);
 }
 
 static int ensure_events(abfs_traversal *t, size_t n) {

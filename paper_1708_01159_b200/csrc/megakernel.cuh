@@ -108,7 +108,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
         break;
     case 3:
-        pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, P.words);
+        pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, 0, P.words);
         grid.sync();
         pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
         break;

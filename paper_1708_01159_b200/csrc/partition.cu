@@ -1,0 +1,479 @@
+// partition.cu -- 1-D vertex-partitioned level-synchronous BFS.
+//
+// Rank p owns the contiguous destination range [lo, hi) (lo a multiple of
+// 32, so its bitmap words [lo/32, ceil(hi/32)) are whole words) and holds:
+//   * the destination-filtered out-CSR over ALL sources: for every u the
+//     out-edges u -> v with v in [lo, hi) (a contiguous sub-range of u's sorted
+//     adjacency, found by two binary searches) -- push / push-warp / edge-list;
+//   * the in-CSR rows and reverse slots of its owned vertices -- pull /
+//     rev-edge-list;
+//   * owned depths, owned visited bitmap, and a REPLICATED global frontier
+//     bitmap (V/8 bytes) plus a global frontier queue built from it.
+// Per level: [bitmap -> queue if the strategy is top-down] -> the strategy
+// kernels on the local slice (the same device functions as the single-GPU
+// engine; depth/visited/bitmap pointers are rebased so they index by global
+// id) -> a pack kernel writes the rank's next-frontier slice (visited bits
+// gained this level) into the caller's send buffer.  The caller all-gathers
+// the send buffers (NCCL over NVLink, or a device concat for partitions
+// sharing one GPU) and abfs_part_exchange unpacks the padded slices into
+// the global next-frontier bitmap, counting it with popc: every rank gets
+// the same global count, hence the same features and the same tree choice.
+//
+// Semantics equal the single-GPU engine from init_depths (consistent state):
+// each owned vertex is claimed by its owner only, exactly once.
+
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.cuh"
+
+using namespace abfs;
+
+struct abfs_part {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t n = 0, lo = 0, hi = 0, wlo = 0, whi = 0, W = 0, nv = 0, nwl = 0, mf = 0, mr = 0;
+    uint32_t *fo_off = nullptr, *fo_dst = nullptr, *fo_org = nullptr;   // filtered forward
+    uint32_t *r_off = nullptr, *r_src = nullptr, *r_own = nullptr;      // owned reverse rows
+    int32_t *depth = nullptr;                                            // [nv]
+    uint32_t *visited = nullptr, *vprev = nullptr, *noin = nullptr, *fnext = nullptr;  // [nwl]
+    uint32_t *fbm[2] = {nullptr, nullptr};                               // global [W]
+    uint32_t *q = nullptr;                                               // global frontier queue
+    uint32_t *qn = nullptr;                                              // local discoveries
+    uint2 *units = nullptr;
+    Ctr *dctr = nullptr;
+    Mailbox *dmb = nullptr;
+    unsigned long long *dres = nullptr, *hres = nullptr;   // {global count, local count}
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int cur = 0;
+    bool has_q = false;
+    uint64_t F = 0;
+    uint64_t call = 0;
+    uint64_t launches = 0;
+    int last_kernel = -1;
+    int last_out = 0;
+};
+
+namespace {
+
+constexpr int kMaxRanks = 64;
+
+struct Bounds {
+    uint64_t w[kMaxRanks + 1];   // global word bounds of the ranks' slices
+    uint32_t P;
+};
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__ a, uint32_t b,
+                                                    uint32_t e, uint32_t key) {
+    while (b < e) {
+        const uint32_t mid = b + ((e - b) >> 1);
+        if (__ldg(a + mid) < key) b = mid + 1;
+        else e = mid;
+    }
+    return b;
+}
+
+// Per source u: the filtered adjacency is dst[start[u] .. start[u]+cnt[u]).
+__global__ void k_part_fcount(const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst,
+                              uint64_t n, uint32_t lo, uint32_t hi, uint32_t *cnt, uint32_t *start) {
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = __ldg(out_off + u), e = __ldg(out_off + u + 1);
+        const uint32_t j0 = lower_bound_u32(dst, b, e, lo);
+        const uint32_t j1 = lower_bound_u32(dst, j0, e, hi);
+        cnt[u] = j1 - j0;
+        start[u] = j0;
+    }
+}
+
+// Edge-parallel copy of the filtered forward slots (keeps (origin, dest) order).
+__global__ void k_part_fcopy(const uint32_t *__restrict__ org, const uint32_t *__restrict__ dst,
+                             uint64_t m, const uint32_t *__restrict__ start,
+                             const uint32_t *__restrict__ fo_off, uint32_t lo, uint32_t hi,
+                             uint32_t *fo_dst, uint32_t *fo_org) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = __ldg(dst + e);
+        if (v < lo || v >= hi) continue;
+        const uint32_t u = __ldg(org + e);
+        const uint32_t pos = __ldg(fo_off + u) + (uint32_t)(e - __ldg(start + u));
+        fo_dst[pos] = v;
+        fo_org[pos] = u;
+    }
+}
+
+__global__ void k_part_roff(const uint32_t *__restrict__ in_off, uint64_t lo, uint64_t nv,
+                            uint32_t base, uint32_t *r_off) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nv;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        r_off[i] = __ldg(in_off + lo + i) - base;
+}
+
+// Local in-degree-0 bitmap; padding bits (local index >= nv) set.
+__global__ void k_part_noin(const uint32_t *__restrict__ r_off, uint64_t nv, uint64_t nwl,
+                            uint32_t *noin) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nwl;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint64_t i = k * 32 + b;
+            if (i >= nv || r_off[i + 1] == r_off[i]) bits |= 1u << b;
+        }
+        noin[k] = bits;
+    }
+}
+
+// init_depths (kernels.py:134-140) on the owned slice + global frontier {root}.
+__global__ void k_part_init(int32_t *depth, uint64_t nv, uint32_t *visited, uint32_t *vprev,
+                            uint64_t nwl, uint32_t *fbm, uint64_t W, uint32_t *q, uint64_t lo,
+                            uint64_t hi, uint32_t root) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    const bool owned = root >= lo && root < hi;
+    for (uint64_t i = tid; i < nv; i += nt) depth[i] = (owned && i == root - lo) ? 0 : kInf;
+    for (uint64_t k = tid; k < nwl; k += nt) {
+        const uint32_t bits = (owned && k == (root - lo) >> 5) ? 1u << ((root - lo) & 31) : 0u;
+        visited[k] = bits;
+        vprev[k] = bits;
+    }
+    for (uint64_t w = tid; w < W; w += nt) fbm[w] = (w == (root >> 5)) ? 1u << (root & 31) : 0u;
+    if (tid == 0) q[0] = root;
+}
+
+// Next-frontier slice = visited bits gained this level; padded to stride.
+__global__ void k_part_pack(const uint32_t *__restrict__ visited, uint32_t *vprev, uint64_t nwl,
+                            uint32_t *send, uint64_t stride) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < stride;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t x = 0;
+        if (k < nwl) {
+            const uint32_t v = visited[k];
+            x = v & ~vprev[k];
+            vprev[k] = v;
+        }
+        send[k] = x;
+    }
+}
+
+// Gathered padded slices -> global next-frontier bitmap, popc -> count.
+__global__ void __launch_bounds__(kBlock)
+k_part_unpack(const uint32_t *__restrict__ gathered, Bounds b, uint64_t stride, uint32_t *fbm,
+              uint64_t W, unsigned long long *res, const unsigned *qlen,
+              const unsigned long long *count) {
+    unsigned long long c = 0;
+    uint32_t r = 0;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < W;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        while (r + 1 < b.P && w >= b.w[r + 1]) ++r;   // w only grows per thread
+        const uint32_t x = __ldg(gathered + (uint64_t)r * stride + (w - b.w[r]));
+        fbm[w] = x;
+        c += __popc(x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(res, c);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        res[1] = qlen ? (unsigned long long)*qlen : *count;
+}
+
+}  // namespace
+
+extern "C" void abfs_part_destroy(abfs_part *p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    void *dev[] = {p->fo_off, p->fo_dst, p->fo_org, p->r_off, p->r_src, p->r_own, p->depth,
+                   p->visited, p->vprev, p->noin, p->fnext, p->fbm[0], p->fbm[1], p->q,
+                   p->qn, p->units, p->dctr, p->dmb, p->dres};
+    for (void *x : dev) cudaFree(x);
+    if (p->hres) cudaFreeHost(p->hres);
+    if (p->e0) cudaEventDestroy(p->e0);
+    if (p->e1) cudaEventDestroy(p->e1);
+    if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+}
+
+extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part **out) {
+    if (!g || !out) return fail(ABFS_EINVAL, "null argument");
+    const uint64_t n = g->d.n, m = g->d.m;
+    if (lo > hi || hi > n) return fail(ABFS_EINVAL, "partition range out of bounds");
+    if (lo % 32) return fail(ABFS_EINVAL, "partition start must be a multiple of 32");
+    if (hi % 32 && hi != n) return fail(ABFS_EINVAL, "partition end must be a multiple of 32 or |V|");
+    ABFS_CUDA(cudaSetDevice(g->device));
+    abfs_part *p = new abfs_part();
+    p->device = g->device;
+    p->n = n;
+    p->lo = lo;
+    p->hi = hi;
+    p->nv = hi - lo;
+    p->wlo = lo / 32;
+    p->whi = (hi + 31) / 32;
+    p->nwl = p->whi - p->wlo;
+    p->W = (n + 31) / 32;
+    cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) p->own_stream = true;
+    cudaStream_t s = p->stream;
+    auto A = [&](void **ptr, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(ptr, bytes ? bytes : 4);
+    };
+    // ---- forward slice: counts, offsets, copy ----------------------------
+    uint32_t *cnt = nullptr, *start = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    A((void **)&cnt, (n + 1) * 4);
+    A((void **)&start, (n + 1) * 4);
+    A((void **)&p->fo_off, (n + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt + n, 0, 4, s);
+    if (e == cudaSuccess && n) {
+        k_part_fcount<<<grid_for(n, kBlock, 148 * 64), kBlock, 0, s>>>(g->d.out_off, g->d.dst, n,
+                                                                       (uint32_t)lo, (uint32_t)hi, cnt, start);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, p->fo_off, (int64_t)(n + 1), s);
+    A(&tmp, tmp_bytes);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, p->fo_off, (int64_t)(n + 1), s);
+    uint32_t mf = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&mf, p->fo_off + n, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    p->mf = mf;
+    A((void **)&p->fo_dst, (uint64_t)mf * 4);
+    A((void **)&p->fo_org, (uint64_t)mf * 4);
+    if (e == cudaSuccess && m) {
+        k_part_fcopy<<<148 * 16, kBlock, 0, s>>>(g->d.org, g->d.dst, m, start, p->fo_off, (uint32_t)lo,
+                                                 (uint32_t)hi, p->fo_dst, p->fo_org);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(cnt);
+    cudaFree(start);
+    cudaFree(tmp);
+    // ---- reverse rows of the owned vertices (contiguous) -----------------
+    uint32_t rb = 0, re = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&rb, g->d.in_off + lo, 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&re, g->d.in_off + hi, 4, cudaMemcpyDeviceToHost);
+    p->mr = (uint64_t)re - rb;
+    A((void **)&p->r_off, (p->nv + 1) * 4);
+    A((void **)&p->r_src, p->mr * 4);
+    A((void **)&p->r_own, p->mr * 4);
+    if (e == cudaSuccess && p->mr)
+        e = cudaMemcpyAsync(p->r_src, g->d.src + rb, p->mr * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && p->mr)
+        e = cudaMemcpyAsync(p->r_own, g->d.rev_owner + rb, p->mr * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) {
+        k_part_roff<<<grid_for(p->nv + 1, kBlock, 148 * 64), kBlock, 0, s>>>(g->d.in_off, lo, p->nv, rb,
+                                                                             p->r_off);
+        e = cudaGetLastError();
+    }
+    // ---- traversal state ---------------------------------------------------
+    const uint64_t wpad = p->nwl + 4;
+    A((void **)&p->depth, (p->nv + 4) * 4);
+    A((void **)&p->visited, wpad * 4);
+    A((void **)&p->vprev, wpad * 4);
+    A((void **)&p->noin, wpad * 4);
+    A((void **)&p->fnext, wpad * 4);
+    A((void **)&p->fbm[0], (p->W + 4) * 4);
+    A((void **)&p->fbm[1], (p->W + 4) * 4);
+    A((void **)&p->q, (n + 4) * 4);
+    A((void **)&p->qn, (p->nv + 4) * 4);
+    const uint64_t mx = p->mf > p->mr ? p->mf : p->mr;
+    A((void **)&p->units, (mx / kHeavy + 64) * sizeof(uint2));
+    A((void **)&p->dctr, sizeof(Ctr));
+    A((void **)&p->dmb, sizeof(Mailbox));
+    A((void **)&p->dres, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&p->hres, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s);
+    if (e == cudaSuccess && p->nwl) {
+        k_part_noin<<<grid_for(p->nwl, kBlock, 148 * 64), kBlock, 0, s>>>(p->r_off, p->nv, p->nwl, p->noin);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventCreate(&p->e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&p->e1);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error(std::string("part_create: ") + cudaGetErrorString(e));
+        abfs_part_destroy(p);
+        return e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA;
+    }
+    *out = p;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_info(const abfs_part *p, uint64_t *lo, uint64_t *hi, uint64_t *m_fwd,
+                              uint64_t *m_rev) {
+    if (!p) return fail(ABFS_EINVAL, "null partition");
+    if (lo) *lo = p->lo;
+    if (hi) *hi = p->hi;
+    if (m_fwd) *m_fwd = p->mf;
+    if (m_rev) *m_rev = p->mr;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_set_stream(abfs_part *p, void *stream) {
+    if (!p) return fail(ABFS_EINVAL, "null partition");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    ABFS_CUDA(cudaStreamSynchronize(p->stream));
+    if (p->own_stream) cudaStreamDestroy(p->stream);
+    if (stream) {
+        p->stream = (cudaStream_t)stream;
+        p->own_stream = false;
+    } else {
+        ABFS_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->own_stream = true;
+    }
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_init(abfs_part *p, int64_t root) {
+    if (!p) return fail(ABFS_EINVAL, "null partition");
+    if (root < 0 || (uint64_t)root >= p->n)
+        return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
+                                     std::to_string(p->n));
+    ABFS_CUDA(cudaSetDevice(p->device));
+    const uint64_t items = p->W > p->nv ? p->W : p->nv;
+    k_part_init<<<grid_for(items, kBlock, 148 * 32), kBlock, 0, p->stream>>>(
+        p->depth, p->nv, p->visited, p->vprev, p->nwl, p->fbm[0], p->W, p->q, p->lo, p->hi,
+        (uint32_t)root);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), p->stream));
+    p->cur = 0;
+    p->has_q = true;
+    p->F = 1;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_level(abfs_part *p, int64_t level, int kernel, int variant,
+                               int64_t chunk, uint32_t *send, uint64_t stride) {
+    if (!p || !send) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
+    if (stride < p->nwl) return fail(ABFS_EINVAL, "send stride smaller than the owned slice");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    ABFS_CUDA(cudaEventRecord(p->e0, s));
+    const bool need_queue = (kernel == ABFS_VERTEX_PUSH || kernel == ABFS_VERTEX_PUSH_WARP);
+    if (need_queue && !p->has_q) {
+        k_bitmap_to_queue<<<grid_for(p->W, kBlock, 1ull << 31), kBlock, 0, s>>>(p->fbm[p->cur], p->W,
+                                                                                p->q, &p->dctr->cq);
+        p->launches += 1;
+        p->has_q = true;
+    }
+    const int out = (int)(p->call % 3);
+    const unsigned long long seq = ++p->call;
+    LevelCtx c;
+    c.depth = p->depth - p->lo;          // rebased: indexed by global id in [lo, hi)
+    c.visited = p->visited - p->wlo;
+    c.fbm = p->fbm[p->cur];
+    c.q_next = p->qn;
+    c.q_tail = &p->dctr->qlen[out];
+    c.count = &p->dctr->count[out];
+    c.units_tail = &p->dctr->units[out];
+    c.units = p->units;
+    c.inconsistent = &p->dctr->inconsistent;
+    c.ctr = p->dctr;
+    c.mb = p->dmb;
+    c.es = nullptr;
+    c.work = &p->dctr->work[out];
+    c.pull_light = kPullLight;
+    c.seq = seq;
+    c.zero_slot = (int)(seq % 3);
+    c.level = (int32_t)level;
+    c.lvl1 = (int32_t)(level + 1);
+    StratArgs a;
+    a.out_off = p->fo_off;
+    a.dst = p->fo_dst;
+    a.org = p->fo_org;
+    a.m_fwd = p->mf;
+    a.in_off = p->r_off - p->lo;
+    a.src = p->r_src;
+    a.rev_owner = p->r_own;
+    a.m_rev = p->mr;
+    a.noin = p->noin - p->wlo;
+    a.fbm_next = p->fnext - p->wlo;
+    a.word0 = p->wlo;
+    a.word_end = p->whi;
+    a.q = p->q;
+    a.F = (uint32_t)p->F;
+    switch (variant) {
+    case 0: p->launches += launch_strategy_args<0>(c, a, kernel, chunk, s); break;
+    case 1: p->launches += launch_strategy_args<1>(c, a, kernel, chunk, s); break;
+    default: p->launches += launch_strategy_args<2>(c, a, kernel, chunk, s); break;
+    }
+    ABFS_CUDA(cudaGetLastError());
+    k_part_pack<<<grid_for(stride, kBlock, 148 * 16), kBlock, 0, s>>>(p->visited, p->vprev, p->nwl,
+                                                                      send, stride);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
+    p->last_kernel = kernel;
+    p->last_out = out;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_exchange(abfs_part *p, const uint32_t *gathered, const uint64_t *word_bounds,
+                                  uint32_t nranks, uint64_t stride, uint64_t *global_count,
+                                  uint64_t *local_count, uint64_t *elapsed_ns) {
+    if (!p || !gathered || !word_bounds || !global_count) return fail(ABFS_EINVAL, "null argument");
+    if (p->last_kernel < 0) return fail(ABFS_EINVAL, "exchange without a level");
+    if (nranks < 1 || nranks > kMaxRanks) return fail(ABFS_EINVAL, "bad rank count");
+    Bounds b;
+    std::memset(&b, 0, sizeof(b));
+    b.P = nranks;
+    bool mine = false;
+    for (uint32_t r = 0; r <= nranks; ++r) b.w[r] = word_bounds[r];
+    for (uint32_t r = 0; r < nranks; ++r) {
+        if (b.w[r] > b.w[r + 1] || b.w[r + 1] - b.w[r] > stride)
+            return fail(ABFS_EINVAL, "bad word bounds / stride");
+        mine |= b.w[r] == p->wlo && b.w[r + 1] == p->whi;
+    }
+    if (b.w[0] != 0 || b.w[nranks] != p->W || !mine)
+        return fail(ABFS_EINVAL, "word bounds do not tile the bitmap around this partition");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    ABFS_CUDA(cudaMemsetAsync(p->dres, 0, 2 * sizeof(unsigned long long), s));
+    const bool topdown = p->last_kernel != ABFS_VERTEX_PULL;
+    k_part_unpack<<<grid_for(p->W, kBlock, 148 * 8), kBlock, 0, s>>>(
+        gathered, b, stride, p->fbm[p->cur ^ 1], p->W, p->dres,
+        topdown ? &p->dctr->qlen[p->last_out] : nullptr, topdown ? nullptr : &p->dctr->count[p->last_out]);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaEventRecord(p->e1, s));
+    ABFS_CUDA(cudaMemcpyAsync(p->hres, p->dres, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    *global_count = p->hres[0];
+    if (local_count) *local_count = p->hres[1];
+    if (elapsed_ns) {
+        float ms = 0.f;
+        ABFS_CUDA(cudaEventElapsedTime(&ms, p->e0, p->e1));
+        const uint64_t ns = (uint64_t)((double)ms * 1e6 + 0.5);
+        *elapsed_ns = ns ? ns : 1;
+    }
+    p->cur ^= 1;
+    p->F = p->hres[0];
+    p->has_q = false;
+    p->last_kernel = -1;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_read_depths(abfs_part *p, int32_t *host_owned) {
+    if (!p || !host_owned) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    ABFS_CUDA(cudaMemcpyAsync(host_owned, p->depth, p->nv * 4, cudaMemcpyDeviceToHost, p->stream));
+    ABFS_CUDA(cudaStreamSynchronize(p->stream));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_depths_device(abfs_part *p, int32_t *dev_out) {
+    if (!p || !dev_out) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    ABFS_CUDA(cudaMemcpyAsync(dev_out, p->depth, p->nv * 4, cudaMemcpyDeviceToDevice, p->stream));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_launches(const abfs_part *p, uint64_t *launches) {
+    if (!p || !launches) return fail(ABFS_EINVAL, "null argument");
+    *launches = p->launches;
+    return ABFS_OK;
+}

@@ -1,0 +1,97 @@
+"""GPU parity of the 1-D vertex-partitioned BFS: P partitions
+of one graph on one B200 (the exchange is a device concat; across GPUs it is
+the NCCL all-gather over the same buffers) reproduce the reference's golden
+depths, per-level counts and adaptive traces for every (kernel, variant),
+and equal the single-GPU engine on larger device-generated graphs."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as G
+import paper_1708_01159_b200 as P
+from paper_1708_01159_b200 import DeviceGraph, Traversal
+from paper_1708_01159_b200.features import static_vector
+from paper_1708_01159_b200.graph import stats_from_offsets
+from paper_1708_01159_b200.partition import LocalExchange, PartitionedBFS, local_partitions
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MODEL = os.path.join(ROOT, "models", "gpu_tree.tree")
+
+
+def make_bfs(dg, parts):
+    stream = torch.cuda.current_stream().cuda_stream
+    ps, bounds = local_partitions(dg, parts, stream)
+    return PartitionedBFS(ps, bounds, LocalExchange(torch),
+                          alloc=lambda s: torch.zeros(s, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", ["kron10", "kron12", "u1000", "er12", "mesh64", "hand1",
+                                  "unreach", "dup", "selfloop", "star7", "single", "path9"])
+def test_partitions_all_pairs_match_golden(name, parts):
+    n, m, a = G.graph_arrays(name)
+    g = P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS])
+    dg = DeviceGraph.upload(g)
+    bfs = make_bfs(dg, parts)
+    stats = stats_from_offsets(n, m, a["out_offsets"], a["in_offsets"])
+    traces = G.traces()["small"]
+    for r in G.roots(name):
+        want = G.depth(name, r)
+        cnt = G.counts(name, r).tolist()
+        for k, v in P.ALL_PAIRS:
+            outs = bfs.bfs_full(r, k, v)
+            assert [o.new_frontier_count for o in outs] == cnt, (name, parts, r, k, v)
+            assert [sum(x) for x in bfs.last_local_counts] == cnt, (name, parts, r, k, v)
+            np.testing.assert_array_equal(bfs.depths(), want, err_msg=f"{name} {parts} {r} {k} {v}")
+        for key, tree in G.trees_for(name):
+            tr = bfs.adaptive(r, P.deserialize(G.tree_path(tree)), stats)
+            got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                   for x in tr.records]
+            assert got == traces[name][str(r)][key], (name, parts, r, key)
+            np.testing.assert_array_equal(bfs.depths(), want)
+
+
+@pytest.mark.parametrize("cfg,parts", [("k18", 8), ("er18", 4), ("mesh256", 3)])
+def test_partitions_equal_single_gpu_engine(cfg, parts):
+    if cfg.startswith("k"):
+        dg = DeviceGraph.rmat(18, 16 << 18, 1, symmetrize=True)
+    elif cfg.startswith("er"):
+        dg = DeviceGraph.uniform(1 << 18, 32 << 18, 1)
+    else:
+        dg = DeviceGraph.mesh(256, 256)
+    stats = P.compute_stats(dg)
+    flat = P.deserialize(MODEL)
+    t = Traversal(dg)
+    bfs = make_bfs(dg, parts)
+    oo, _ = dg.offsets()
+    cand = np.flatnonzero(np.diff(oo.astype(np.int64)) > 0)
+    for r in [int(cand[0]), int(cand[len(cand) // 2]), int(cand[-1])]:
+        want = np.empty(dg.vertex_count, np.int32)
+        recs = t.adaptive(r, flat.as_abfs(), static_vector(stats), 32, depths_out=want)
+        tr = bfs.adaptive(r, flat, stats)
+        assert [(int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size)
+                for x in tr.records] == \
+               [(x.kernel, x.variant, x.fallback, x.frontier_size) for x in recs]
+        np.testing.assert_array_equal(bfs.depths(), want)
+        for k, v in [(P.KernelId.VERTEX_PUSH_WARP, P.CountVariant.TWO_LEVEL_REDUCE),
+                     (P.KernelId.REV_EDGE_LIST, P.CountVariant.GROUP_REDUCE)]:
+            outs = bfs.bfs_full(r, k, v)
+            assert sum(o.new_frontier_count for o in outs) + 1 == int((want != G.INF).sum())
+            np.testing.assert_array_equal(bfs.depths(), want)
+
+
+def test_partition_rejects_misaligned_range():
+    n, m, a = G.graph_arrays("kron10")
+    dg = DeviceGraph.upload(P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS]))
+    from paper_1708_01159_b200.partition import DevicePartition
+    with pytest.raises(ValueError, match="multiple of 32"):
+        DevicePartition(dg, 5, 64)
+    with pytest.raises(ValueError, match="out of bounds"):
+        DevicePartition(dg, 0, n + 1)
