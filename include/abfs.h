@@ -204,6 +204,8 @@ ABFS_API int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part
 ABFS_API void abfs_part_destroy(abfs_part *p);
 ABFS_API int abfs_part_info(const abfs_part *p, uint64_t *lo, uint64_t *hi, uint64_t *m_fwd,
                             uint64_t *m_rev);
+/* The stream the partition enqueues on, used as given: NULL is the legacy
+ * default stream (a new partition owns a private stream). */
 ABFS_API int abfs_part_set_stream(abfs_part *p, void *cuda_stream);
 /* init_depths (kernels.py:134-140) on the owned slice; frontier = {root}. */
 ABFS_API int abfs_part_init(abfs_part *p, int64_t root);

@@ -317,13 +317,10 @@ extern "C" int abfs_part_set_stream(abfs_part *p, void *stream) {
     ABFS_CUDA(cudaSetDevice(p->device));
     ABFS_CUDA(cudaStreamSynchronize(p->stream));
     if (p->own_stream) cudaStreamDestroy(p->stream);
-    if (stream) {
-        p->stream = (cudaStream_t)stream;
-        p->own_stream = false;
-    } else {
-        ABFS_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-        p->own_stream = true;
-    }
+    // taken as given, NULL included (= the legacy default stream, which is
+    // torch's default stream: the exchange must be ordered with torch ops)
+    p->stream = (cudaStream_t)stream;
+    p->own_stream = false;
     return ABFS_OK;
 }
 
