@@ -329,6 +329,124 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def run_partitioned(a):
+    """--partition: config 3 -- one tree-switched BFS over a 1-D vertex
+    partition (edge-balanced destination ranges, one rank per GPU, frontier
+    bitmap slices all-gathered over NCCL every level).  At N=1,
+    --virtual-parts P runs P partitions on the one GPU (device concat)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1708_01159_b200 as P
+    from paper_1708_01159_b200 import DeviceGraph
+    from paper_1708_01159_b200.partition import (DevicePartition, DistExchange, LocalExchange,
+                                                 PartitionedBFS, edge_balanced_bounds)
+
+    rank, world, local = env_rank()
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    parts_n = world if world > 1 else max(1, a.virtual_parts)
+    t_setup = time.time()
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        dg = DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev)
+        V, E = dg.vertex_count, dg.edge_count
+        oo, io = dg.offsets()
+        stats = P.compute_stats(dg)
+        bounds = edge_balanced_bounds(io, parts_n)
+        mine = [rank] if world > 1 else list(range(parts_n))
+        parts = [DevicePartition(dg, int(bounds[i]), int(bounds[i + 1]), stream.cuda_stream)
+                 for i in mine]
+        dg.close()
+        exch = DistExchange(torch, dist) if world > 1 else LocalExchange(torch)
+        bfs = PartitionedBFS(parts, bounds, exch,
+                             alloc=lambda s: torch.zeros(s, dtype=torch.int32, device=f"cuda:{dev}"))
+        flat = P.deserialize(a.model)
+        roots = pick_roots(oo, 64, seed=1)
+        deg = np.diff(oo.astype(np.int64))
+        order = [roots[i % len(roots)] for i in range(a.warmup + a.steps)]
+        m_trav, levels = {}, {}
+        for r in sorted(set(order)):
+            tr = bfs.adaptive(r, flat, stats)
+            d = bfs.depths()
+            m_trav[r] = float(deg[d != 2**31 - 1].sum()) / 2
+            levels[r] = tr.level_count
+        setup_s = time.time() - t_setup
+        for r in order[:a.warmup]:
+            bfs.adaptive(r, flat, stats)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        l0 = sum(p.launches() for p in parts)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        edges, nlev = 0.0, 0
+        with ClockSampler(dev) as clk:
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for r in order[a.warmup:]:
+                bfs.adaptive(r, flat, stats)
+                edges += m_trav[r]
+                nlev += levels[r]
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        launches = sum(p.launches() for p in parts) - l0
+        ms = exch.max_over_ranks(ev0.elapsed_time(ev1))
+        gteps = edges / (ms * 1e-3) / 1e9
+        # exchange share (untimed replay with all-gather events)
+        bfs.time_exchange = True
+        for r in order[a.warmup:a.warmup + min(4, a.steps)]:
+            bfs.adaptive(r, flat, stats)
+        bfs.time_exchange = False
+        ex_ms = exch.max_over_ranks(bfs.exchange_ms / max(1, bfs.exchange_calls))
+        recv = (parts_n - 1) * bfs.stride * 4
+        # e2e: the partitioned call + gathered host depths
+        t0 = time.perf_counter()
+        ne = min(4, a.steps)
+        e_edges = 0.0
+        for r in order[a.warmup:a.warmup + ne]:
+            bfs.adaptive(r, flat, stats)
+            bfs.depths()
+            e_edges += m_trav[r]
+        torch.cuda.synchronize()
+        e_el = exch.max_over_ranks(time.perf_counter() - t0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator)",
+            "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS, "
+                                   f"1-D vertex partition",
+                       "scale": a.scale, "vertices": V, "directed_edge_slots": E,
+                       "partitions": parts_n, "roots_per_step": 1,
+                       "parallelism": (f"1-D edge-balanced vertex partition over {world} GPUs, "
+                                       "NCCL all-gather of frontier bitmap slices per level")
+                       if world > 1 else f"{parts_n} partitions on one GPU (device concat)",
+                       "model": os.path.relpath(a.model, ROOT),
+                       "l2": "inputs larger than L2"},
+            "gpu_launches": int(launches),
+            "exchange": {"bytes_received_per_rank_per_level": int(recv),
+                         "mean_allgather_us": round(ex_ms * 1e3, 2),
+                         "GBps_received_per_rank": round(recv / (ex_ms * 1e-3) / 1e9, 2)
+                         if ex_ms > 0 else None,
+                         "nvlink_peak_GBps_per_direction": 900.0,
+                         "levels_timed": nlev},
+            "e2e": {"value": round(e_edges / e_el / 1e9, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": 8, "d2h_bytes_per_step": int(4 * V),
+                    "api": "PartitionedBFS.adaptive + depths() (gathered host int32 depths)"},
+            "cpu_baseline": None,
+            "clocks": clk.summary(),
+            "setup_s": round(setup_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    for p in parts:
+        p.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def cpu_baseline(dg, roots, model, static24, budget_s):
     """The reference algorithm's CPU port (oracle/) on the host cores, same
     graph / tree / roots, bounded to ~budget_s seconds (>= 1 root)."""
@@ -420,19 +538,27 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--scale", type=int, default=None)
     ap.add_argument("--roots-per-step", type=int, default=4)
     ap.add_argument("--model", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--partition", action="store_true",
+                    help="config 3: one BFS over a 1-D vertex partition (default scale 26)")
+    ap.add_argument("--virtual-parts", type=int, default=8,
+                    help="--partition at N=1: partitions sharing the one GPU")
     ap.add_argument("--mode", type=int, default=1,
                     help="1: device-resident level loop (megakernel); 0: per-level launches")
     a = ap.parse_args()
     a.model = os.path.abspath(a.model) if a.model else default_model()
     if a.warmup < 3:
         a.warmup = 3
+    if a.scale is None:
+        a.scale = 26 if a.partition else 24
     if a.impl == "reference":
         run_reference(a)
+    elif a.partition:
+        run_partitioned(a)
     else:
         run_ours(a)
 

@@ -86,6 +86,7 @@ constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 256;      // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 1024;      // edges per CTA work unit (4 steps of 256)
+constexpr uint32_t kPushHub = 64;     // vertex push: degree above -> CTA units
 constexpr uint32_t kPullLight = 32;   // pull phase A default (ABFS_PULL_LIGHT overrides)
 constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
 
@@ -104,7 +105,8 @@ __device__ __forceinline__ void zero_slot(const LevelCtx &c) {
 // Last CTA to finish publishes (qlen, count) to the mapped mailbox.  Must be
 // reached by every thread of every CTA of the level's final kernel.
 __device__ __forceinline__ void publish(const LevelCtx &c) {
-    __threadfence();   // every thread's counter atomics are performed before the ticket
+    // the CTA barrier orders every thread's counter atomics before thread
+    // 0's (cumulative) gpu-scope fence, so one fence per CTA suffices
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -151,6 +153,33 @@ __device__ __forceinline__ bool claim(const LevelCtx &c, uint32_t v, bool consis
     if (old != kInf) return false;
     atomicOr(w, bit);
     return true;
+}
+
+// Four candidates at once: the visited-word loads, then the atomics, are
+// issued back to back (4 independent L2 round trips in flight instead of a
+// chain of 4).  Same outcome as four claim() calls in order: a vertex
+// repeated within the batch is won at most once.
+__device__ __forceinline__ void claim4(const LevelCtx &c, const uint32_t (&v)[4],
+                                       const bool (&act)[4], bool (&won)[4], bool consistent) {
+    if (!consistent) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) won[k] = act[k] && claim(c, v[k], false);
+        return;
+    }
+    uint32_t wv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) wv[k] = act[k] ? c.visited[v[k] >> 5] : 0xffffffffu;
+    uint32_t old[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t bit = 1u << (v[k] & 31);
+        old[k] = (wv[k] & bit) ? bit : atomicOr(c.visited + (v[k] >> 5), bit);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        won[k] = act[k] && !(old[k] & (1u << (v[k] & 31)));
+        if (won[k]) c.depth[v[k]] = c.lvl1;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -368,7 +397,11 @@ k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
 
 // ---------------------------------------------------------------------------
 // VERTEX_PUSH (run_level_vertex_push + _push_block, kernels.py:234-267):
-// one thread per frontier vertex walks its out-adjacency in order.
+// one thread per frontier vertex walks its out-adjacency in order.  A
+// vertex of degree > kPushHub is not walked by one thread (a Kronecker hub
+// has ~10^5-10^6 edges: one thread would serialise the whole level); its
+// adjacency is queued as kUnit-edge CTA work units for k_heavy, exactly as
+// in push-warp.  Semantics are unchanged (same claims, same counts).
 // ---------------------------------------------------------------------------
 template <int VAR>
 __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
@@ -384,16 +417,25 @@ __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
             const uint32_t u = __ldg(q + i);
             j = __ldg(out_off + u);
             e = __ldg(out_off + u + 1);
+            if (e - j > kPushHub) {
+                const uint32_t nu = (e - j + kUnit - 1) / kUnit;
+                const uint32_t s = atomicAdd(c.units_tail, nu);
+                for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(u, k);
+                j = e;
+            }
         }
         while (__any_sync(kFull, j < e)) {
-            bool won = false;
-            uint32_t v = 0;
-            if (j < e) {
-                v = __ldg(dst + j);
-                ++j;
-                won = claim(c, v, consistent);
+            uint32_t v[4];
+            bool act[4], won[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                act[k] = j + k < e;
+                v[k] = act[k] ? __ldg(dst + j + k) : 0u;
             }
-            em.emit(won, v);
+            j = min(e, j + 4);
+            claim4(c, v, act, won, consistent);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
         }
         em.tile_end();
     }
@@ -407,7 +449,6 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
     __shared__ SmemQ sq;
     zero_slot(c);
     push_body<VAR>(c, &sq, q, F, out_off, dst);
-    publish(c);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,14 +489,17 @@ __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
             }
         }
         while (__any_sync(kFull, j < e)) {
-            bool won = false;
-            uint32_t v = 0;
-            if (j < e) {
-                v = __ldg(dst + j);
-                j += VW;
-                won = claim(c, v, consistent);
+            uint32_t v[4];
+            bool act[4], won[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                act[k] = j + k * VW < e;
+                v[k] = act[k] ? __ldg(dst + j + k * VW) : 0u;
             }
-            em.emit(won, v);
+            j += 4 * VW;
+            claim4(c, v, act, won, consistent);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
         }
         em.tile_end();
     }
@@ -482,15 +526,18 @@ __device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
         const uint2 un = c.units[w];
         const uint32_t b = __ldg(out_off + un.x) + un.y * kUnit;
         const uint32_t e = min(__ldg(out_off + un.x + 1), b + kUnit);
-        for (uint32_t jb = b; jb < e; jb += kBlock) {
-            const uint32_t j = jb + threadIdx.x;
-            bool won = false;
-            uint32_t v = 0;
-            if (j < e) {
-                v = __ldg(dst + j);
-                won = claim(c, v, consistent);
+        for (uint32_t jb = b; jb < e; jb += kBlock * 4) {
+            uint32_t v[4];
+            bool act[4], won[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t j = jb + k * kBlock + threadIdx.x;
+                act[k] = j < e;
+                v[k] = act[k] ? __ldg(dst + j) : 0u;
             }
-            em.emit(won, v);
+            claim4(c, v, act, won, consistent);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
         }
         em.tile_end();
     }
@@ -508,136 +555,166 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // ---------------------------------------------------------------------------
 // VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): unvisited
 // vertices scan their in-neighbours and stop at the first frontier vertex.
-// A warp takes a tile of 32 bitmap words; fully settled words (visited or
-// in-degree 0) cost one coalesced load and store.  For a word with work the
-// warp owns its 32 vertices:
-//   first kPullLight entries  every lane scans its own list, 4 loads in flight
-//   rest <= kPullHeavy        the whole warp scans the list 128 at a time
+// A warp takes a tile of 32 bitmap words (one atomic fetch) and walks it in
+// sub-tiles of 8 words (256 vertices).  Fully settled words (visited or
+// in-degree 0) cost one load and one store.  The candidates of a sub-tile
+// (unvisited, in-degree > 0) are compacted into a per-warp shared-memory
+// list, then processed 32 at a time, one lane per candidate, so every lane
+// carries a real vertex (a word with 3 candidates no longer idles 29 lanes
+// through a chain of dependent loads):
+//   first pull_light entries  each lane scans its own list, 4 loads in flight
+//   rest <= kPullHeavy        the warp scans the pending remainders together,
+//                             128 entries per step (load balanced)
 //   rest larger               kUnit-edge CTA units (k_pull_heavy)
-// with early exit on the first frontier in-neighbour in every case.  The
-// warp owns its visited / next-frontier words, so they are written without
-// atomics, and every next-frontier word is written (no clearing pass).
+// with early exit on the first frontier in-neighbour in every case.  Found
+// bits gather in a per-warp shared word array; the warp owns its visited /
+// next-frontier words, so they are written without global atomics, and every
+// next-frontier word is written (no clearing pass).
 // ---------------------------------------------------------------------------
+constexpr int kPullSub = 8;                  // words per sub-tile
+constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
+
 template <int VAR>
 __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ in_off,
                                           const uint32_t *__restrict__ src,
                                           const uint32_t *__restrict__ noin,
                                           uint32_t *__restrict__ fbm_next, uint64_t word0,
-                                          uint64_t words) {
+                                          uint64_t words, uint32_t *wbuf, uint32_t *wfound) {
     // words [word0, words) of the bitmaps (a vertex partition passes its
-    // owned range; bitmap/offset pointers are indexed by global ids)
+    // owned range; bitmap/offset pointers are indexed by global ids);
+    // wbuf = kPullList entries, wfound = kPullSub words, both per warp
     CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
-    const unsigned lt_mask = (1u << lane) - 1u;
     const uint64_t ntiles = (words - word0 + 31) / 32;
     unsigned long long scanned = 0;
     for (;;) {
-        // dynamic tile fetch: one atomic per warp per 32-word tile
         unsigned long long tile = 0;
         if (lane == 0) tile = atomicAdd(c.work, 1ull);
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= ntiles) break;
-        const uint64_t myw = word0 + tile * 32 + lane;
-        uint32_t vis = 0xffffffffu, skip = 0xffffffffu;
-        if (myw < words) {
-            vis = c.visited[myw];
-            skip = vis | __ldg(noin + myw);
-        }
-        unsigned need = __ballot_sync(kFull, skip != 0xffffffffu);
-        if (myw < words && skip == 0xffffffffu) fbm_next[myw] = 0u;
-        while (need) {
-            const int wl = __ffs(need) - 1;
-            need &= need - 1;
-            const uint64_t word = word0 + tile * 32 + wl;
-            const uint32_t wvis = __shfl_sync(kFull, vis, wl);
-            const uint32_t wskip = __shfl_sync(kFull, skip, wl);
-            const uint64_t v = word * 32 + lane;
-            const bool cand = !((wskip >> lane) & 1u);   // padding bits are set in noin
-            uint32_t j = 0, e = 0;
-            if (cand) {
-                j = __ldg(in_off + v);
-                e = __ldg(in_off + v + 1);
+        for (int sub = 0; sub < 32 / kPullSub; ++sub) {
+            const uint64_t wbase = word0 + tile * 32 + (uint64_t)sub * kPullSub;
+            if (wbase >= words) break;
+            const uint64_t myw = wbase + lane;
+            const bool mine = lane < (unsigned)kPullSub && myw < words;
+            uint32_t vis = 0xffffffffu, cand = 0;
+            if (mine) {
+                vis = c.visited[myw];
+                cand = ~(vis | __ldg(noin + myw));   // padding bits are set in noin
+                if (!cand) fbm_next[myw] = 0u;
+                wfound[lane] = 0u;
             }
-            // phase A: each candidate scans up to c.pull_light of its own
-            // in-neighbours, 4 independent loads per step (early exit)
-            bool found = false;
-            const uint32_t ja = min(e, j + c.pull_light);
-            while (__any_sync(kFull, j < ja)) {
-                if (j < ja) {
-                    const uint32_t jb = min(ja, j + 4);
-                    scanned += jb - j;
-                    const uint32_t u0 = __ldg(src + j);
-                    const uint32_t u1 = j + 1 < jb ? __ldg(src + j + 1) : u0;
-                    const uint32_t u2 = j + 2 < jb ? __ldg(src + j + 2) : u0;
-                    const uint32_t u3 = j + 3 < jb ? __ldg(src + j + 3) : u0;
-                    if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
-                        in_bitmap(c.fbm, u3)) {
-                        found = true;
-                        j = e;
-                    } else {
-                        j = jb;
-                    }
+            // compact the candidates of the sub-tile into wbuf (vertex order)
+            const uint32_t cnt = __popc(cand);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < kPullSub; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= (unsigned)o) incl += t;
+            }
+            const uint32_t total = __shfl_sync(kFull, incl, kPullSub - 1);
+            if (!total) continue;
+            {
+                uint32_t pos = incl - cnt, bits = cand;
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    wbuf[pos++] = (uint32_t)(myw * 32 + b);
                 }
             }
-            // super-heavy remainders go to CTA units (k_pull_heavy)
-            bool pend = !found && j < e;
-            if (pend && e - j > kPullHeavy) {
-                const uint32_t nu = (e - j + kUnit - 1) / kUnit;
-                const uint32_t s = atomicAdd(c.units_tail, nu);
-                for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2((uint32_t)v, k);
-                pend = false;
-            }
-            // phase B: the warp walks the concatenation of all pending
-            // remainders 128 entries per step (load-balanced, mostly
-            // coalesced), skipping owners already found, until every pending
-            // vertex has a frontier in-neighbour or the lists are exhausted
-            const unsigned pmask = __ballot_sync(kFull, pend);
-            if (pmask) {
-                const uint32_t rem = pend ? e - j : 0u;
-                uint32_t incl = rem;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= (unsigned)o) incl += t;
+            __syncwarp();
+            for (uint32_t base = 0; base < total; base += 32) {
+                const bool has = base + lane < total;
+                const uint32_t v = has ? wbuf[base + lane] : 0u;
+                uint32_t j = 0, e = 0;
+                if (has) {
+                    j = __ldg(in_off + v);
+                    e = __ldg(in_off + v + 1);
                 }
-                const uint32_t excl = incl - rem;
-                const uint32_t total = __shfl_sync(kFull, incl, 31);
-                unsigned fmask = 0;
-                for (uint32_t base = 0; base < total; base += 128) {
-                    unsigned hit_bits = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t p = base + k * 32 + lane;
-                        // owner = last lane whose exclusive offset <= p
-                        int owner = 0;
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1) {
-                            const uint32_t ex = __shfl_sync(kFull, excl, owner + step);
-                            if (ex <= p) owner += step;
-                        }
-                        const uint32_t oj = __shfl_sync(kFull, j, owner);
-                        const uint32_t oex = __shfl_sync(kFull, excl, owner);
-                        if (p < total && !((fmask >> owner) & 1u)) {
-                            ++scanned;
-                            if (in_bitmap(c.fbm, __ldg(src + oj + (p - oex)))) hit_bits |= 1u << owner;
+                // phase A: each candidate scans up to pull_light of its own
+                // in-neighbours, 4 independent loads per step (early exit)
+                bool found = false;
+                const uint32_t ja = min(e, j + c.pull_light);
+                while (__any_sync(kFull, j < ja)) {
+                    if (j < ja) {
+                        const uint32_t jb = min(ja, j + 4);
+                        scanned += jb - j;
+                        const uint32_t u0 = __ldg(src + j);
+                        const uint32_t u1 = j + 1 < jb ? __ldg(src + j + 1) : u0;
+                        const uint32_t u2 = j + 2 < jb ? __ldg(src + j + 2) : u0;
+                        const uint32_t u3 = j + 3 < jb ? __ldg(src + j + 3) : u0;
+                        if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
+                            in_bitmap(c.fbm, u3)) {
+                            found = true;
+                            j = e;
+                        } else {
+                            j = jb;
                         }
                     }
-                    fmask |= __reduce_or_sync(kFull, hit_bits);
-                    if ((fmask & pmask) == pmask) break;
                 }
-                found |= (fmask >> lane) & 1u;
+                // super-heavy remainders go to CTA units (k_pull_heavy)
+                bool pend = !found && j < e;
+                if (pend && e - j > kPullHeavy) {
+                    const uint32_t nu = (e - j + kUnit - 1) / kUnit;
+                    const uint32_t s = atomicAdd(c.units_tail, nu);
+                    for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(v, k);
+                    pend = false;
+                }
+                // phase B: the warp walks the concatenation of all pending
+                // remainders 128 entries per step, skipping owners already
+                // found, until every pending owner is found or exhausted
+                const unsigned pmask = __ballot_sync(kFull, pend);
+                if (pmask) {
+                    const uint32_t rem = pend ? e - j : 0u;
+                    uint32_t inc2 = rem;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(kFull, inc2, o);
+                        if (lane >= (unsigned)o) inc2 += t;
+                    }
+                    const uint32_t excl = inc2 - rem;
+                    const uint32_t tot2 = __shfl_sync(kFull, inc2, 31);
+                    unsigned fmask = 0;
+                    for (uint32_t b2 = 0; b2 < tot2; b2 += 128) {
+                        unsigned hit_bits = 0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t p = b2 + k * 32 + lane;
+                            // owner = last lane whose exclusive offset <= p
+                            int owner = 0;
+#pragma unroll
+                            for (int step = 16; step > 0; step >>= 1) {
+                                const uint32_t ex = __shfl_sync(kFull, excl, owner + step);
+                                if (ex <= p) owner += step;
+                            }
+                            const uint32_t oj = __shfl_sync(kFull, j, owner);
+                            const uint32_t oex = __shfl_sync(kFull, excl, owner);
+                            if (p < tot2 && !((fmask >> owner) & 1u)) {
+                                ++scanned;
+                                if (in_bitmap(c.fbm, __ldg(src + oj + (p - oex)))) hit_bits |= 1u << owner;
+                            }
+                        }
+                        fmask |= __reduce_or_sync(kFull, hit_bits);
+                        if ((fmask & pmask) == pmask) break;
+                    }
+                    found |= (fmask >> lane) & 1u;
+                }
+                if (found) {
+                    c.depth[v] = c.lvl1;
+                    atomicOr(wfound + ((v >> 5) - wbase), 1u << (v & 31));
+                }
+                em.add(__ballot_sync(kFull, found));
             }
-            const unsigned fm = __ballot_sync(kFull, found);
-            if (found) c.depth[v] = c.lvl1;
-            if (lane == 0) {
-                fbm_next[word] = fm;
-                if (fm) c.visited[word] = wvis | fm;
+            __syncwarp();
+            if (mine && cand) {
+                const uint32_t fm = wfound[lane];
+                fbm_next[myw] = fm;
+                if (fm) c.visited[myw] = vis | fm;
             }
-            em.add(fm);
+            __syncwarp();
         }
     }
-    (void)lt_mask;
     em.finish();
     if (c.es) {
 #pragma unroll
@@ -646,14 +723,22 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
     }
 }
 
+// Per-warp scratch of pull_body inside one CTA.
+struct SmemPull {
+    uint32_t list[kWarps][kPullList];
+    uint32_t found[kWarps][kPullSub];
+};
+
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
        const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t word0,
        uint64_t words) {
     __shared__ unsigned int sn;
+    __shared__ SmemPull sp;
     zero_slot(c);
-    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, word0, words);
+    const unsigned w = threadIdx.x >> 5;
+    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, word0, words, sp.list[w], sp.found[w]);
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit

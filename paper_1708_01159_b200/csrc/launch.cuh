@@ -73,7 +73,8 @@ static int launch_strategy_args(const LevelCtx &c, const StratArgs &a, int kerne
         return 1;
     case ABFS_VERTEX_PUSH:
         k_push<VAR><<<grid_for(a.F, kBlock, 148 * 64), kBlock, 0, s>>>(c, a.q, a.F, a.out_off, a.dst);
-        return 1;
+        k_heavy<VAR><<<148 * 8, kBlock, 0, s>>>(c, a.out_off, a.dst);
+        return 2;
     case ABFS_VERTEX_PULL:
         k_pull<VAR><<<grid_for(a.word_end - a.word0, kBlock, 148 * 64), kBlock, 0, s>>>(
             c, a.in_off, a.src, a.noin, a.fbm_next, a.word0, a.word_end);

@@ -96,7 +96,7 @@ template <int VAR>
 __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
                                               uint32_t F, const uint32_t *q, uint32_t *fbm_next,
                                               SmemQ *sq, unsigned *sn, int *s_done,
-                                              cg::grid_group &grid) {
+                                              uint32_t *pfound, cg::grid_group &grid) {
     switch (kernel) {
     case 0:
         edge_body<VAR, false, 1>(c, sq, P.org, P.dst, P.m);
@@ -106,9 +106,17 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         break;
     case 2:
         push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
+        grid.sync();
+        heavy_body<VAR>(c, sq, P.out_off, P.dst);
         break;
     case 3:
-        pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, 0, P.words);
+        {
+            // the pull scratch lists alias the (idle) CTA queue buffer
+            static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");
+            const unsigned w = threadIdx.x >> 5;
+            pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, 0, P.words,
+                           sq->buf + w * kPullList, pfound + w * kPullSub);
+        }
         grid.sync();
         pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
         break;
@@ -126,6 +134,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
 template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
+    __shared__ uint32_t pfound[kWarps * kPullSub];
     __shared__ unsigned sn;
     __shared__ int s_done;
     __shared__ int s_cls;
@@ -223,9 +232,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
         switch (pv) {
-        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
-        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
-        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, grid); break;
+        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
+        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
+        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
         }
         const bool topdown = pk != 3;
         const unsigned long long nw = topdown

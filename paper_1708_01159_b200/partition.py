@@ -212,13 +212,26 @@ class PartitionedBFS:
         self.sends = [alloc(self.stride) for _ in self.parts]
         self.stream = stream
         self.last_local_counts: list[list[int]] = []
+        # optional: CUDA-event time of the all-gathers (bench NVLink figure)
+        self.time_exchange = False
+        self.exchange_ms = 0.0
+        self.exchange_calls = 0
 
     # -- one level ------------------------------------------------------------
     def _level(self, level: int, kernel: int, variant: int, chunk: int):
         for p, s in zip(self.parts, self.sends):
             p.level(level, kernel, variant, chunk, s)
+        if self.time_exchange:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         gathered = self.exchange.allgather(self.sends)
+        if self.time_exchange:
+            ev[1].record()
         res = [p.exchange(gathered, self.wbounds, self.stride) for p in self.parts]
+        if self.time_exchange:
+            self.exchange_ms += ev[0].elapsed_time(ev[1])
+            self.exchange_calls += 1
         counts = {r[0] for r in res}
         if len(counts) != 1:
             raise RuntimeError(f"partitions disagree on the level count: {sorted(counts)}")

@@ -77,3 +77,33 @@ def test_config3_kronecker26_single_gpu():
     dg = DeviceGraph.rmat(26, 16 << 26, 1, symmetrize=True)
     assert dg.edge_count == 1 << 31
     check_graph(dg, [1], [(4, 2)], symmetric=False)
+
+
+def test_config3_kronecker26_partitioned_8():
+    """Config 3's 1-D vertex partition (8 edge-balanced ranges, exchanged by
+    device concat on one GPU -- the same buffers NCCL all-gathers across
+    GPUs) equals the single-GPU engine: traces and depths."""
+    import torch
+
+    from paper_1708_01159_b200.partition import LocalExchange, PartitionedBFS, local_partitions
+    dg = DeviceGraph.rmat(26, 16 << 26, 1, symmetrize=True)
+    stats = P.compute_stats(dg)
+    flat = P.deserialize(MODEL)
+    want = {}
+    t = Traversal(dg)
+    for r in (1, 123457):
+        d = np.empty(dg.vertex_count, np.int32)
+        recs = t.adaptive(r, flat.as_abfs(), static_vector(stats), 32, depths_out=d)
+        want[r] = (d, [(x.kernel, x.variant, x.fallback, x.frontier_size) for x in recs])
+    t.close()
+    ps, bounds = local_partitions(dg, 8, torch.cuda.current_stream().cuda_stream)
+    dg.close()
+    bfs = PartitionedBFS(ps, bounds, LocalExchange(torch),
+                         alloc=lambda s: torch.zeros(s, dtype=torch.int32, device="cuda"))
+    for r, (d, tr) in want.items():
+        got = bfs.adaptive(r, flat, stats)
+        assert [(int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size)
+                for x in got.records] == tr
+        np.testing.assert_array_equal(bfs.depths(), d)
+    for p in ps:
+        p.close()
