@@ -633,19 +633,22 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                     e = __ldg(in_off + v + 1);
                 }
                 // phase A: each candidate scans up to pull_light of its own
-                // in-neighbours, 4 independent loads per step (early exit)
+                // in-neighbours one aligned 16-byte load per step (one L1
+                // wavefront per lane instead of four), early exit
                 bool found = false;
                 const uint32_t ja = min(e, j + c.pull_light);
                 while (__any_sync(kFull, j < ja)) {
                     if (j < ja) {
-                        const uint32_t jb = min(ja, j + 4);
+                        const uint32_t b4 = j & ~3u;
+                        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(src + b4));
+                        const uint32_t jb = min(ja, b4 + 4);
                         scanned += jb - j;
-                        const uint32_t u0 = __ldg(src + j);
-                        const uint32_t u1 = j + 1 < jb ? __ldg(src + j + 1) : u0;
-                        const uint32_t u2 = j + 2 < jb ? __ldg(src + j + 2) : u0;
-                        const uint32_t u3 = j + 3 < jb ? __ldg(src + j + 3) : u0;
-                        if (in_bitmap(c.fbm, u0) | in_bitmap(c.fbm, u1) | in_bitmap(c.fbm, u2) |
-                            in_bitmap(c.fbm, u3)) {
+                        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+                        bool hit = false;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (b4 + k >= j && b4 + k < jb) hit |= in_bitmap(c.fbm, xs[k]);
+                        if (hit) {
                             found = true;
                             j = e;
                         } else {

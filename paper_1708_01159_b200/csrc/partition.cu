@@ -257,7 +257,7 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     if (e == cudaSuccess) e = cudaMemcpy(&re, g->d.in_off + hi, 4, cudaMemcpyDeviceToHost);
     p->mr = (uint64_t)re - rb;
     A((void **)&p->r_off, (p->nv + 1) * 4);
-    A((void **)&p->r_src, p->mr * 4);
+    A((void **)&p->r_src, p->mr * 4 + 16);   // +16: aligned 16-byte reads in pull
     A((void **)&p->r_own, p->mr * 4);
     if (e == cudaSuccess && p->mr)
         e = cudaMemcpyAsync(p->r_src, g->d.src + rb, p->mr * 4, cudaMemcpyDeviceToDevice, s);
