@@ -97,6 +97,7 @@ def main():
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
     traffic = {}
+    last_level = None
     for rep in a.rep:
         recs = summarise(rep)
         lines += [f"## `{rep.split('/')[-1]}` (`ncu --set full --clock-control none`)", "",
@@ -106,12 +107,18 @@ def main():
             lines.append(f"| {r['kernel']} | {r.get('grid','')} | {r.get('regs','')} | {r.get('time',0):.1f} | "
                          f"{r.get('dram_rd',0)/1e6:.1f} | {r.get('dram_wr',0)/1e6:.1f} | {r.get('dram_%',0):.1f} | "
                          f"{r.get('L2_hit_%',0):.1f} | {r.get('L1_hit_%',0):.1f} | {r.get('warps_active_%',0):.1f} | {r['top_stalls']} |")
-            key = {"k_pull": "VERTEX_PULL", "k_push_warp": "VERTEX_PUSH_WARP", "k_heavy": "VERTEX_PUSH_WARP",
+            # one entry per LEVEL: the second kernel of a level (the CTA-unit
+            # pass k_pull_heavy / k_heavy) adds to the entry its level opened
+            base = r["kernel"].split("<")[0].split("::")[-1]
+            byt = r.get("dram_rd", 0) + r.get("dram_wr", 0)
+            key = {"k_pull": "VERTEX_PULL", "k_push_warp": "VERTEX_PUSH_WARP",
                    "k_edge": "EDGE_LIST", "k_push": "VERTEX_PUSH"}
-            for pre, kname in key.items():
-                if r["kernel"].split("<")[0].endswith(pre):
-                    traffic.setdefault(kname, []).append(r.get("dram_rd", 0) + r.get("dram_wr", 0))
-                    break
+            if base in ("k_pull_heavy", "k_heavy"):
+                if last_level is not None:
+                    traffic[last_level][-1] += byt
+            elif base in key:
+                last_level = key[base]
+                traffic.setdefault(last_level, []).append(byt)
         lines.append("")
     for path in a.launches:
         agg = launches(path)
@@ -126,7 +133,7 @@ def main():
     if a.traffic and traffic:
         with open(a.traffic, "w") as fh:
             json.dump({k: {"bytes_per_launch_mean": sum(v) / len(v), "launches": len(v),
-                           "source": "ncu --set full of the standalone launch-path kernel"}
+                           "source": "ncu --set full of the launch-path kernels of each level (strategy kernel + its CTA-unit pass), tree-switched run of the bench roots"}
                        for k, v in traffic.items()}, fh, indent=1)
     print("\n".join(lines))
 
