@@ -97,6 +97,11 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
                                               uint32_t F, const uint32_t *q, uint32_t *fbm_next,
                                               SmemQ *sq, unsigned *sn, int *s_done,
                                               uint32_t *pfound, cg::grid_group &grid) {
+    // Two-phase strategies (light pass, then CTA work units) need a second
+    // barrier only if the light pass created units: after the first barrier
+    // every CTA reads the same unit count, and with none the level's count
+    // is already final (saves a grid barrier on most small levels).
+    const auto units = [&]() { return *(volatile unsigned *)c.units_tail; };
     switch (kernel) {
     case 0:
         edge_body<VAR, false, 1>(c, sq, P.org, P.dst, P.m);
@@ -107,6 +112,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
     case 2:
         push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
         grid.sync();
+        if (!units()) return;
         heavy_body<VAR>(c, sq, P.out_off, P.dst);
         break;
     case 3:
@@ -118,11 +124,13 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
                            sq->buf + w * kPullList, pfound + w * kPullSub);
         }
         grid.sync();
+        if (!units()) return;
         pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
         break;
     default:
         push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2);
         grid.sync();
+        if (!units()) return;
         heavy_body<VAR>(c, sq, P.out_off, P.dst);
         break;
     }
