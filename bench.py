@@ -209,14 +209,17 @@ def run_ours(a):
     ev1 = torch.cuda.Event(enable_timing=True)
     edges = 0.0
     bfs_ns = 0
+    per_root = []
     with ClockSampler(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for s in range(a.warmup, a.warmup + a.steps):
             for r in order[s * R:(s + 1) * R]:
                 trav.adaptive(r, tree, static24, 32)
-                bfs_ns += trav.last_ns()
+                ns_r = trav.last_ns()
+                bfs_ns += ns_r
                 edges += m_trav[r]
+                per_root.append(m_trav[r] / (ns_r * 1e-9) / 1e9)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = trav.launches() - launches0
@@ -274,6 +277,37 @@ def run_ours(a):
                 "whole_traversal_GBps": round(sum(v[1] for v in per_kernel.values()) /
                                               (total_ns * 1e-9) / 1e9, 1)}
 
+    # ---- every fixed pair vs the switched run (same roots, untimed extra) ----
+    from types import SimpleNamespace as NS
+    sample = my_roots[:max(1, min(len(my_roots), a.fixed_roots))]
+    fixed = {}
+    sw_ns, sw_e = 0, 0.0
+    for r in sample:
+        trav.adaptive(r, tree, static24, 32)
+        sw_ns += trav.last_ns()
+        sw_e += m_trav[r]
+    for k, v in P.ALL_PAIRS:
+        ns_tot, e_tot = 0, 0.0
+        for r in sample:
+            trav.bfs_full(r, int(k), int(v), 32)
+            ns_tot += trav.last_ns()
+            e_tot += m_trav[r]
+        trav.instrument(True)
+        _, el = trav.bfs_full(sample[0], int(k), int(v), 32)
+        wm = work_model(trav, [NS(kernel=int(k), variant=int(v), elapsed_ns=int(x), converted=False)
+                               for x in el], V, E)
+        trav.instrument(False)
+        byt, t_ns = sum(x[3] for x in wm), sum(x[2] for x in wm)
+        fixed[f"{k.name}/{v.name}"] = {"gteps": round(e_tot / (ns_tot * 1e-9) / 1e9, 3),
+                                       "roofline_frac": round(byt / (t_ns * 1e-9) / 1e9 / peak, 4)}
+    best_fixed = max(fixed, key=lambda x: fixed[x]["gteps"])
+    sw_gteps = sw_e / (sw_ns * 1e-9) / 1e9
+    fixed_block = {"roots": len(sample), "basis": "device time after init_depths (t_bfs)",
+                   "switched_gteps": round(sw_gteps, 3), "best_fixed": best_fixed,
+                   "best_fixed_gteps": fixed[best_fixed]["gteps"],
+                   "switched_over_best_fixed": round(sw_gteps / fixed[best_fixed]["gteps"], 3),
+                   "pairs": fixed}
+
     # ---- e2e through the public API with host results ----------------------
     e2e = None
     if rank == 0 or world > 1:
@@ -316,6 +350,10 @@ def run_ours(a):
                        "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
                        "l2": "inputs larger than L2 (graph arrays 8.1 GB)"},
             "gteps_graph500_tbfs": round(edges / (bfs_ns * 1e-9) / 1e9, 3) if world == 1 else None,
+            "gteps_per_root": {"median": round(statistics.median(per_root), 3),
+                               "harmonic_mean": round(len(per_root) / sum(1 / x for x in per_root), 3),
+                               "bfs": len(per_root)} if per_root else None,
+            "fixed_vs_switched": fixed_block,
             "gpu_launches": int(launches),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -535,7 +573,7 @@ def run_reference(a):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=None)
@@ -543,6 +581,8 @@ def main():
     ap.add_argument("--model", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--fixed-roots", type=int, default=4,
+                    help="roots for the per-pair fixed-variant comparison")
     ap.add_argument("--partition", action="store_true",
                     help="config 3: one BFS over a 1-D vertex partition (default scale 26)")
     ap.add_argument("--virtual-parts", type=int, default=8,
