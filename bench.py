@@ -199,8 +199,7 @@ def run_ours(a):
     R = a.roots_per_step
     order = [my_roots[i % len(my_roots)] for i in range(R * (a.warmup + a.steps))]
     for s in range(a.warmup):
-        for r in order[s * R:(s + 1) * R]:
-            trav.adaptive(r, tree, static24, 32)
+        trav.adaptive_batch(order[s * R:(s + 1) * R], tree, static24, 32)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -214,9 +213,10 @@ def run_ours(a):
         torch.cuda.synchronize()
         ev0.record(stream)
         for s in range(a.warmup, a.warmup + a.steps):
-            for r in order[s * R:(s + 1) * R]:
-                trav.adaptive(r, tree, static24, 32)
-                ns_r = trav.last_ns()
+            # one step = one batched launch: R tree-switched BFSs back to back
+            batch = order[s * R:(s + 1) * R]
+            _, ns_b, _ = trav.adaptive_batch(batch, tree, static24, 32)
+            for r, ns_r in zip(batch, ns_b.tolist()):
                 bfs_ns += ns_r
                 edges += m_trav[r]
                 per_root.append(m_trav[r] / (ns_r * 1e-9) / 1e9)
@@ -345,6 +345,8 @@ def run_ours(a):
             "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
                        "scale": a.scale, "vertices": V, "directed_edge_slots": E,
                        "roots_per_step": R, "roots_pool": 64,
+                       "step": "abfs_adaptive_bfs_batch: R tree-switched BFSs (init_depths "
+                               "included) in one persistent launch",
                        "level_loop": "device (persistent megakernel)" if a.mode else "host (per-level launches)",
                        "model": os.path.relpath(a.model, ROOT),
                        "parallelism": f"roots sharded over {world} GPU(s), graph replicated",

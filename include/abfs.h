@@ -165,6 +165,18 @@ ABFS_API int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree 
                       int32_t *depths_out, abfs_level_record *records,
                       size_t cap, size_t *n_levels);
 
+/* Multi-source throughput form of adaptive_bfs (no reference counterpart;
+ * each traversal has adaptive.py:83-129 semantics): nroots (<= 4096)
+ * tree-switched BFSs run back to back inside ONE persistent launch, each
+ * root's init_depths inside the kernel, no host round trip between them.
+ * levels[i] / bfs_ns[i] (optional) = level calls and device time (first
+ * level start .. last level end) of root i; total_ns = the launch.  The
+ * depth array afterwards holds the last root's traversal. */
+ABFS_API int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, size_t nroots,
+                                     const abfs_tree *tree, const double *static24,
+                                     int64_t chunk_size, uint64_t *levels, uint64_t *bfs_ns,
+                                     uint64_t *total_ns);
+
 /* Total device time (ns) of the last abfs_bfs_full/abfs_adaptive_bfs call,
  * from after init_depths to the final count readback. */
 ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);

@@ -75,6 +75,9 @@ _SIGNATURES = {
                                          ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64, i32p,
                                          ctypes.POINTER(AbfsLevelRecord), ctypes.c_size_t,
                                          ctypes.POINTER(ctypes.c_size_t)]),
+    "abfs_adaptive_bfs_batch": (ctypes.c_int, [ctypes.c_void_p, i64p, ctypes.c_size_t,
+                                               ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
+                                               u64p, u64p, u64p]),
     "abfs_last_traversal_ns": (ctypes.c_int, [ctypes.c_void_p, u64p]),
     "abfs_traversal_set_mode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "abfs_traversal_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),

@@ -68,8 +68,11 @@ struct abfs_traversal {
     MegaRecord *mrecs = nullptr;         // host-mapped level records (written by the kernel)
     MegaRecord *drecs = nullptr;         // device view of mrecs
     std::vector<MegaRecord> hrecs;
-    unsigned long long *mnlev = nullptr, *dnlev = nullptr;   // host-mapped level count
+    unsigned long long *mnlev = nullptr, *dnlev = nullptr;   // host-mapped level counts (per root)
+    uint32_t *hroots = nullptr, *droots = nullptr;            // batch roots (pinned / device)
     std::vector<unsigned char> last_blob;                    // tree blob resident on the device
+    std::vector<unsigned long long> batch_levels;            // per-root level counts, last launch
+    size_t batch_recs = 0;                                   // records kept in mrecs, last launch
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
     int mega_grid = 0;
@@ -319,6 +322,8 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->des);
     if (t->mrecs) cudaFreeHost(t->mrecs);
     if (t->mnlev) cudaFreeHost(t->mnlev);
+    if (t->hroots) cudaFreeHost(t->hroots);
+    cudaFree(t->droots);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
     if (t->stage) cudaFreeHost(t->stage);
@@ -463,8 +468,14 @@ static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // Run a whole traversal in the persistent cooperative kernel.  fixed_pair
 // >= 0 runs bfs_full with that pair; otherwise the tree picks per level.
-static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_tree *tr,
-                    const double *static24, int64_t chunk, size_t *n_levels) {
+constexpr size_t kMaxBatch = 4096;         // roots per batched megakernel launch
+
+// roots: nroots >= 1 traversals run back to back in one launch; with
+// host_init the host ran init_depths for the single root, otherwise every
+// root's init runs inside the kernel.  n_levels = the last root's level count.
+static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, bool host_init,
+                    int fixed_pair, const abfs_tree *tr, const double *static24, int64_t chunk,
+                    size_t *n_levels) {
     const DevGraph &g = t->g->d;
     cudaStream_t s = t->stream;
     ABFS_CUDA(cudaSetDevice(t->device));
@@ -473,10 +484,16 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
         // write per level), so a traversal needs a single stream sync
         ABFS_CUDA(cudaHostAlloc((void **)&t->mrecs, kMegaCap * sizeof(MegaRecord), cudaHostAllocMapped));
         ABFS_CUDA(cudaHostGetDevicePointer((void **)&t->drecs, t->mrecs, 0));
-        ABFS_CUDA(cudaHostAlloc((void **)&t->mnlev, sizeof(unsigned long long), cudaHostAllocMapped));
+        ABFS_CUDA(cudaHostAlloc((void **)&t->mnlev, kMaxBatch * sizeof(unsigned long long),
+                                cudaHostAllocMapped));
         ABFS_CUDA(cudaHostGetDevicePointer((void **)&t->dnlev, t->mnlev, 0));
+        ABFS_CUDA(cudaMallocHost((void **)&t->hroots, kMaxBatch * sizeof(uint32_t)));
+        ABFS_CUDA(cudaMalloc((void **)&t->droots, kMaxBatch * sizeof(uint32_t)));
     }
-    void *kfn = t->mega_minb == 5 ? (void *)k_mega<5> : (void *)k_mega<6>;
+    if (nroots < 1 || nroots > kMaxBatch) return fail(ABFS_EINVAL, "bad root count");
+    void *kfn = t->mega_minb == 4   ? (void *)k_mega<4>
+                : t->mega_minb == 5 ? (void *)k_mega<5>
+                                    : (void *)k_mega<6>;
     if (!t->mega_grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -517,9 +534,15 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
         ABFS_CUDA(cudaMemcpyAsync(t->dtree, t->htree, bytes, cudaMemcpyHostToDevice, s));
         t->last_blob.swap(blob);
     }
-    ABFS_TRY(init_impl(t, root));
-    ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
-    ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3 + 8 * 3, s));
+    if (host_init) {
+        ABFS_TRY(init_impl(t, roots[0]));
+        ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
+        ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3 + 8 * 3, s));
+    } else {
+        std::memcpy(t->hroots, roots, nroots * sizeof(uint32_t));
+        ABFS_CUDA(cudaMemcpyAsync(t->droots, t->hroots, nroots * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, s));
+    }
     ABFS_TRY(ensure_events(t, 2));
     MegaParams P;
     P.depth = t->depth;
@@ -556,16 +579,26 @@ static int mega_run(abfs_traversal *t, int64_t root, int fixed_pair, const abfs_
     P.cap = kMegaCap;
     P.recs = t->drecs;
     P.n_levels = t->dnlev;
-    *(volatile unsigned long long *)t->mnlev = 0;
+    P.roots = t->droots;
+    P.nroots = (uint32_t)nroots;
+    P.init_in_kernel = host_init ? 0 : 1;
+    for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
     ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
     t->launches += 1;
     ABFS_CUDA(cudaEventRecord(t->ev[1], s));
     ABFS_CUDA(cudaStreamSynchronize(s));
-    const unsigned long long nl = *(volatile unsigned long long *)t->mnlev;
-    const size_t keep = nl < kMegaCap ? nl : kMegaCap;
-    t->hrecs.assign(t->mrecs, t->mrecs + keep);
+    unsigned long long tot = 0;
+    for (size_t i = 0; i < nroots; ++i) tot += ((volatile unsigned long long *)t->mnlev)[i];
+    const unsigned long long nl = ((volatile unsigned long long *)t->mnlev)[nroots - 1];
+    // records of the last root (the batch keeps all roots' records in mrecs)
+    const size_t keep_all = tot < kMegaCap ? tot : kMegaCap;
+    const size_t first = (size_t)(tot - nl) < keep_all ? (size_t)(tot - nl) : keep_all;
+    t->hrecs.assign(t->mrecs + first, t->mrecs + keep_all);
+    const size_t keep = t->hrecs.size();
+    t->batch_levels.assign(t->mnlev, t->mnlev + nroots);
+    t->batch_recs = keep_all;
     float ms = 0.f;
     ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->ev[1]));
     t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
@@ -596,7 +629,7 @@ static uint64_t rec_ns(const MegaRecord &r) {
 extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
     t->use_mega = device_loop != 0;
-    const int minb = device_loop == 2 ? 5 : 6;
+    const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 5 : 6;
     if (minb != t->mega_minb) {
         t->mega_minb = minb;
         t->mega_grid = 0;
@@ -614,7 +647,8 @@ extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int va
             return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
                                          std::to_string(t->g->d.n));
         size_t nl = 0;
-        ABFS_TRY(mega_run(t, root, kernel * 3 + variant, nullptr, nullptr, chunk, &nl));
+        const uint32_t r32 = (uint32_t)root;
+        ABFS_TRY(mega_run(t, &r32, 1, true, kernel * 3 + variant, nullptr, nullptr, chunk, &nl));
         *n_levels = nl;
         for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
             if (counts) counts[l] = t->hrecs[l].new_count;
@@ -715,7 +749,8 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
             return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
                                          std::to_string(t->g->d.n));
         size_t nl = 0;
-        ABFS_TRY(mega_run(t, root, -1, tr, static24, chunk, &nl));
+        const uint32_t r32 = (uint32_t)root;
+        ABFS_TRY(mega_run(t, &r32, 1, true, -1, tr, static24, chunk, &nl));
         *n_levels = nl;
         if (recs)
             for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
@@ -876,5 +911,42 @@ extern "C" int abfs_host_register(void *ptr, size_t bytes) {
 extern "C" int abfs_host_unregister(void *ptr) {
     if (!ptr) return fail(ABFS_EINVAL, "null argument");
     ABFS_CUDA(cudaHostUnregister(ptr));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, size_t nroots,
+                                       const abfs_tree *tr, const double *static24,
+                                       int64_t chunk, uint64_t *levels, uint64_t *bfs_ns,
+                                       uint64_t *total_ns) {
+    if (!t || !roots || !static24) return fail(ABFS_EINVAL, "null argument");
+    if (nroots < 1 || nroots > kMaxBatch)
+        return fail(ABFS_EINVAL, "need 1.." + std::to_string(kMaxBatch) + " roots per batch");
+    ABFS_TRY(tree_ok(tr));
+    ABFS_TRY(level_params_ok(0, 0, 0, chunk));
+    std::vector<uint32_t> r32(nroots);
+    for (size_t i = 0; i < nroots; ++i) {
+        if (roots[i] < 0 || (uint64_t)roots[i] >= t->g->d.n)
+            return fail(ABFS_EINVAL, "root " + std::to_string(roots[i]) + " out of range for |V|=" +
+                                         std::to_string(t->g->d.n));
+        r32[i] = (uint32_t)roots[i];
+    }
+    size_t nl = 0;
+    ABFS_TRY(mega_run(t, r32.data(), nroots, false, -1, tr, static24, chunk, &nl));
+    if (total_ns) *total_ns = t->last_trav_ns;
+    size_t off = 0;
+    for (size_t i = 0; i < nroots; ++i) {
+        const size_t li = (size_t)t->batch_levels[i];
+        if (levels) levels[i] = li;
+        if (bfs_ns) {
+            // t_bfs of root i: first level's start to last level's end
+            uint64_t ns = 0;
+            if (li && off + li <= t->batch_recs) {
+                const MegaRecord &a = t->mrecs[off], &b = t->mrecs[off + li - 1];
+                ns = b.t_end > a.t_start ? b.t_end - a.t_start : 1;
+            }
+            bfs_ns[i] = ns;
+        }
+        off += li;
+    }
     return ABFS_OK;
 }

@@ -48,7 +48,13 @@ struct MegaParams {
     uint32_t pull_light;
     uint32_t cap;
     MegaRecord *recs;
-    unsigned long long *n_levels;
+    unsigned long long *n_levels;   // per root
+    // roots of this launch, traversed one after the other; with init_in_kernel
+    // every root's init_depths runs inside the kernel (else the host did it
+    // for the single root)
+    const uint32_t *roots;
+    uint32_t nroots;
+    int init_in_kernel;
 };
 
 
@@ -169,6 +175,39 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         T.cls = base + P.o_cls;
         T.st = reinterpret_cast<const double *>(base + P.o_st);
     }
+    unsigned long long rec_off = 0;
+    for (uint32_t ri = 0; ri < P.nroots; ++ri) {
+    if (P.init_in_kernel) {
+        // init_depths (kernels.py:134-140) + frontier {root}, as k_init
+        const uint32_t root = P.roots[ri];
+        const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+        const uint64_t nt = (uint64_t)gridDim.x * kBlock;
+        const uint64_t n4 = P.n / 4;
+        const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+        for (uint64_t i = tid; i < n4; i += nt) reinterpret_cast<int4 *>(P.depth)[i] = inf4;
+        for (uint64_t i = n4 * 4 + tid; i < P.n; i += nt) P.depth[i] = kInf;
+        for (uint64_t w = tid; w < P.words; w += nt) {
+            const uint32_t bits = (w == (root >> 5)) ? 1u << (root & 31) : 0u;
+            P.visited[w] = bits;
+            P.fbm0[w] = bits;
+        }
+        grid.sync();
+        if (lead) {
+            P.depth[root] = 0;
+            P.q0[0] = root;
+            for (int s = 0; s < 3; ++s) {
+                P.ctr->qlen[s] = 0;
+                P.ctr->units[s] = 0;
+                P.ctr->count[s] = 0;
+                P.ctr->cq3[s] = 0;
+                P.ctr->es3[s] = 0;
+                P.ctr->work[s] = 0;
+            }
+            P.ctr->cq = 0;
+            P.ctr->inconsistent = 0;
+        }
+        grid.sync();
+    }
     unsigned long long frontier = 1, discovered = 1;
     int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
     int cur = 0;
@@ -248,8 +287,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         const unsigned long long nw = topdown
             ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
             : *(volatile unsigned long long *)&P.ctr->count[out];
-        if (lead && level < P.cap) {
-            MegaRecord &r = P.recs[level];
+        if (lead && rec_off + level < P.cap) {
+            MegaRecord &r = P.recs[rec_off + level];
             r.kernel = pk;
             r.variant = pv;
             r.fallback = fallback;
@@ -262,8 +301,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.scanned = P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;
         }
         if (nw == 0) {
-            if (lead) *P.n_levels = (unsigned long long)level + 1;
-            return;
+            if (lead) P.n_levels[ri] = (unsigned long long)level + 1;
+            rec_off += level + 1;
+            break;
         }
         frontier = nw;
         discovered += nw;
@@ -271,6 +311,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         has_q = topdown;
         has_bm = !topdown;
     }
+    }   // roots
 }
 
 }  // namespace abfs

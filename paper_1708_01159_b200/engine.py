@@ -196,6 +196,21 @@ class Traversal:
             ctypes.byref(nl)), "adaptive_bfs")
         return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:min(nl.value, cap)]]
 
+    def adaptive_batch(self, roots, tree: L.AbfsTree, static24: np.ndarray,
+                       chunk_size: int = 32):
+        """Tree-switched BFS from every root in one persistent launch
+        (abfs_adaptive_bfs_batch): returns (levels, bfs_ns per root, total_ns)."""
+        r = np.ascontiguousarray(roots, dtype=np.int64)
+        lv = np.zeros(r.size, np.uint64)
+        ns = np.zeros(r.size, np.uint64)
+        tot = ctypes.c_uint64()
+        st = np.ascontiguousarray(static24, dtype=np.float64)
+        L.check(L.lib().abfs_adaptive_bfs_batch(self._h, L.ptr(r, L.i64p), r.size, ctypes.byref(tree),
+                                                L.ptr(st, L.f64p), int(chunk_size), L.ptr(lv, L.u64p),
+                                                L.ptr(ns, L.u64p), ctypes.byref(tot)),
+                "adaptive_bfs_batch")
+        return lv, ns, tot.value
+
     def _records(self, cap: int):
         # one record buffer per traversal (allocating 3.6 MB per call would
         # dominate short traversals)

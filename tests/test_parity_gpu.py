@@ -222,3 +222,27 @@ def test_device_loop_and_launch_loop_agree(name):
             assert res[True][2:] == res[False][2:]
     finally:
         t.set_device_loop(True)
+
+
+@pytest.mark.parametrize("name", ["kron12", "u1000", "mesh64", "unreach", "star7"])
+def test_adaptive_batch_matches_single_traversals(name):
+    """abfs_adaptive_bfs_batch: several tree-switched BFSs in one launch
+    (in-kernel init per root) give each root's level count, and the final
+    depth array equals the last root's golden depths."""
+    from paper_1708_01159_b200 import DeviceGraph, Traversal
+    from paper_1708_01159_b200.features import static_vector
+    g = graph(name)
+    dg = DeviceGraph.upload(g)
+    t = Traversal(dg)
+    flat = P.deserialize(G.tree_path("t1"))
+    stats = P.compute_stats(g)
+    roots = G.roots(name)
+    order = roots + roots[::-1]
+    lv, ns, tot = t.adaptive_batch(order, flat.as_abfs(), static_vector(stats))
+    want = [len(G.traces()["small"][name][str(r)]["t1"]) for r in order]
+    assert lv.tolist() == want
+    assert (ns > 0).all() and tot > 0
+    np.testing.assert_array_equal(t.read(), G.depth(name, order[-1]))
+    with pytest.raises(ValueError, match="out of range"):
+        t.adaptive_batch([0, g.vertex_count], flat.as_abfs(), static_vector(stats))
+    t.close()
