@@ -158,6 +158,18 @@ KERNEL_NAMES = ["EDGE_LIST", "REV_EDGE_LIST", "VERTEX_PUSH", "VERTEX_PULL", "VER
 
 
 # ---------------------------------------------------------------------------
+def make_graph(a, dev):
+    """(DeviceGraph, symmetric, workload name) for --graph."""
+    from paper_1708_01159_b200 import DeviceGraph
+    if a.graph == "er":        # config 5: uniform-random, 32M vertices, avg degree 32
+        return (DeviceGraph.uniform(1 << 25, 1 << 30, 1, device=dev), False,
+                "erdos-renyi-32M-deg32 (directed)")
+    if a.graph == "mesh":      # config 4: 4096 x 4096 4-neighbour grid
+        return DeviceGraph.mesh(4096, 4096, device=dev), True, "mesh-4096x4096"
+    return (DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev), True,
+            f"kronecker-{a.scale}-ef16-symmetrised")
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -174,7 +186,7 @@ def run_ours(a):
     torch.cuda.set_device(dev)
 
     t_setup = time.time()
-    dg = DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev)
+    dg, symmetric, wname = make_graph(a, dev)
     V, E = dg.vertex_count, dg.edge_count
     oo, io = dg.offsets()
     stats = P.compute_stats(dg)
@@ -193,7 +205,7 @@ def run_ours(a):
     for r in my_roots:
         trav.adaptive(r, tree, static24, 32)
         e, _ = trav.reached()
-        m_trav[r] = e / 2
+        m_trav[r] = e / 2 if symmetric else float(e)
     setup_s = time.time() - t_setup
 
     R = a.roots_per_step
@@ -334,7 +346,7 @@ def run_ours(a):
     # ---- CPU baseline: oracle port of the reference algorithm --------------
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(dg, roots_all, a.model, static24, a.cpu_seconds)
+        cpu = cpu_baseline(dg, roots_all, a.model, static24, a.cpu_seconds, symmetric)
 
     if rank == 0:
         line = {
@@ -342,8 +354,9 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator)",
-            "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
-                       "scale": a.scale, "vertices": V, "directed_edge_slots": E,
+            "config": {"workload": f"{wname} tree-switched BFS",
+                       "graph": a.graph, "scale": a.scale, "vertices": V, "directed_edge_slots": E,
+                       "teps_basis": "sum of out-degree of reached vertices" + (" / 2" if symmetric else ""),
                        "roots_per_step": R, "roots_pool": 64,
                        "step": "abfs_adaptive_bfs_batch: R tree-switched BFSs (init_depths "
                                "included) in one persistent launch",
@@ -361,7 +374,8 @@ def run_ours(a):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "trace_first_root": trace_pairs,
+            "trace_first_root": {"levels": len(trace_pairs), "first_16": trace_pairs[:16]}
+            if trace_pairs else None,
             "setup_s": round(setup_s, 1),
         }
         print(json.dumps(line), flush=True)
@@ -487,7 +501,7 @@ def run_partitioned(a):
         dist.destroy_process_group()
 
 
-def cpu_baseline(dg, roots, model, static24, budget_s):
+def cpu_baseline(dg, roots, model, static24, budget_s, symmetric=True):
     """The reference algorithm's CPU port (oracle/) on the host cores, same
     graph / tree / roots, bounded to ~budget_s seconds (>= 1 root)."""
     import oracle
@@ -508,12 +522,12 @@ def cpu_baseline(dg, roots, model, static24, budget_s):
         t0 = time.perf_counter()
         d, _ = oracle.adaptive_bfs(og, r, ot, static24, threads=threads)
         el += time.perf_counter() - t0
-        edges += deg[d != 2**31 - 1].sum() / 2
+        edges += deg[d != 2**31 - 1].sum() / (2 if symmetric else 1)
         done += 1
         if el >= budget_s:
             break
     return {"value": round(edges / el / 1e9, 5), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{done} tree-switched BFS root(s) on the full K{int(np.log2(dg.vertex_count))} "
+            "sample": f"{done} tree-switched BFS root(s) on the full {dg.vertex_count}-vertex "
                       f"graph, same tree; C+OpenMP port of the reference level kernels "
                       f"(oracle/abfs_oracle.c), {el:.1f}s wall"}
 
@@ -585,6 +599,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--fixed-roots", type=int, default=4,
                     help="roots for the per-pair fixed-variant comparison")
+    ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er", "mesh"],
+                    help="workload graph (configs 2 / 5 / 4); the headline is kronecker")
     ap.add_argument("--partition", action="store_true",
                     help="config 3: one BFS over a 1-D vertex partition (default scale 26)")
     ap.add_argument("--virtual-parts", type=int, default=8,
