@@ -88,7 +88,10 @@ constexpr uint32_t kHeavy = 256;      // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 1024;      // edges per CTA work unit (4 steps of 256)
 constexpr uint32_t kPushHub = 64;     // vertex push: degree above -> CTA units
 constexpr uint32_t kPullLight = 32;   // pull phase A default (ABFS_PULL_LIGHT overrides)
-constexpr uint32_t kPullHeavy = 4096; // pull: warp scan up to this, CTA units above
+#ifndef ABFS_PULL_HEAVY
+#define ABFS_PULL_HEAVY 256
+#endif
+constexpr uint32_t kPullHeavy = ABFS_PULL_HEAVY;  // pull: warp scan up to this, CTA units above
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
