@@ -393,8 +393,10 @@ def run_partitioned(a):
 
     import paper_1708_01159_b200 as P
     from paper_1708_01159_b200 import DeviceGraph
-    from paper_1708_01159_b200.partition import (DevicePartition, DistExchange, LocalExchange,
-                                                 PartitionedBFS, edge_balanced_bounds)
+    from paper_1708_01159_b200.partition import (DevicePartition, DistExchange,
+                                                 DistPeerExchange, LocalExchange,
+                                                 LocalPeerExchange, PartitionedBFS,
+                                                 edge_balanced_bounds)
 
     rank, world, local = env_rank()
     dev = local if world > 1 else 0
@@ -414,7 +416,11 @@ def run_partitioned(a):
         parts = [DevicePartition(dg, int(bounds[i]), int(bounds[i + 1]), stream.cuda_stream)
                  for i in mine]
         dg.close()
-        exch = DistExchange(torch, dist) if world > 1 else LocalExchange(torch)
+        if a.exchange == "peer":
+            exch = (DistPeerExchange(torch, dist, parts[0]) if world > 1
+                    else LocalPeerExchange(torch, parts))
+        else:
+            exch = DistExchange(torch, dist) if world > 1 else LocalExchange(torch)
         bfs = PartitionedBFS(parts, bounds, exch,
                              alloc=lambda s: torch.zeros(s, dtype=torch.int32, device=f"cuda:{dev}"))
         flat = P.deserialize(a.model)
@@ -448,13 +454,18 @@ def run_partitioned(a):
         launches = sum(p.launches() for p in parts) - l0
         ms = exch.max_over_ranks(ev0.elapsed_time(ev1))
         gteps = edges / (ms * 1e-3) / 1e9
-        # exchange share (untimed replay with all-gather events)
-        bfs.time_exchange = True
-        for r in order[a.warmup:a.warmup + min(4, a.steps)]:
-            bfs.adaptive(r, flat, stats)
-        bfs.time_exchange = False
-        ex_ms = exch.max_over_ranks(bfs.exchange_ms / max(1, bfs.exchange_calls))
-        recv = (parts_n - 1) * bfs.stride * 4
+        # exchange share (untimed replay with all-gather events; the fused
+        # peer exchange has no separate collective to time)
+        ex_ms = 0.0
+        if a.exchange != "peer":
+            bfs.time_exchange = True
+            for r in order[a.warmup:a.warmup + min(4, a.steps)]:
+                bfs.adaptive(r, flat, stats)
+            bfs.time_exchange = False
+            ex_ms = exch.max_over_ranks(bfs.exchange_ms / max(1, bfs.exchange_calls))
+            recv = (parts_n - 1) * bfs.stride * 4
+        else:
+            recv = int((V + 31) // 32 * 4 * (parts_n - 1) / parts_n)
         # e2e: the partitioned call + gathered host depths
         t0 = time.perf_counter()
         ne = min(4, a.steps)
@@ -481,8 +492,10 @@ def run_partitioned(a):
                        "model": os.path.relpath(a.model, ROOT),
                        "l2": "inputs larger than L2"},
             "gpu_launches": int(launches),
-            "exchange": {"bytes_received_per_rank_per_level": int(recv),
-                         "mean_allgather_us": round(ex_ms * 1e3, 2),
+            "exchange": {"kind": "fused peer stores over NVLink + mailbox signal (no collective)"
+                         if a.exchange == "peer" else "NCCL all-gather of padded bitmap slices",
+                         "bytes_received_per_rank_per_level": int(recv),
+                         "mean_allgather_us": round(ex_ms * 1e3, 2) if ex_ms else None,
                          "GBps_received_per_rank": round(recv / (ex_ms * 1e-3) / 1e9, 2)
                          if ex_ms > 0 else None,
                          "nvlink_peak_GBps_per_direction": 900.0,
@@ -603,6 +616,8 @@ def main():
                     help="workload graph (configs 2 / 5 / 4); the headline is kronecker")
     ap.add_argument("--partition", action="store_true",
                     help="config 3: one BFS over a 1-D vertex partition (default scale 26)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="--partition frontier exchange: fused peer stores or NCCL all-gather")
     ap.add_argument("--virtual-parts", type=int, default=8,
                     help="--partition at N=1: partitions sharing the one GPU")
     ap.add_argument("--mode", type=int, default=1,

@@ -237,6 +237,26 @@ ABFS_API int abfs_part_exchange(abfs_part *p, const uint32_t *gathered,
                                 const uint64_t *word_bounds, uint32_t nranks, uint64_t stride,
                                 uint64_t *global_count, uint64_t *local_count,
                                 uint64_t *elapsed_ns);
+/* Fused exchange (no collective): each rank's level ends with a kernel that
+ * stores its next-frontier slice straight into every rank's global bitmap
+ * over NVLink peer memory and signals each rank's mailbox with system-scope
+ * atomics; abfs_part_p2p_finish waits (bounded, ABFS_ENCCL on timeout) for
+ * all ranks' signals and sums their counts.  Peers are given either as
+ * device pointers (partitions of one process, abfs_part_peer_buffers) or
+ * by CUDA IPC handles (one process per GPU: abfs_part_ipc_export fills 192
+ * bytes per rank; abfs_part_ipc_open takes all ranks' handles in rank
+ * order). */
+ABFS_API int abfs_part_peer_buffers(abfs_part *p, void **fbm0, void **fbm1, void **mailbox);
+ABFS_API int abfs_part_set_peers(abfs_part *p, void *const *fbm0, void *const *fbm1,
+                                 void *const *mailboxes, uint32_t nranks, uint32_t rank);
+ABFS_API int abfs_part_ipc_export(abfs_part *p, unsigned char *handles /* 192 bytes */);
+ABFS_API int abfs_part_ipc_open(abfs_part *p, const unsigned char *all_handles, uint32_t nranks,
+                                uint32_t rank);
+ABFS_API int abfs_part_level_p2p(abfs_part *p, int64_t level, int kernel, int variant,
+                                 int64_t chunk_size);
+ABFS_API int abfs_part_p2p_finish(abfs_part *p, uint64_t *global_count, uint64_t *local_count,
+                                  uint64_t *elapsed_ns);
+
 /* Owned depths (hi - lo entries) to host / to a device buffer (async). */
 ABFS_API int abfs_part_read_depths(abfs_part *p, int32_t *host_owned);
 ABFS_API int abfs_part_depths_device(abfs_part *p, int32_t *dev_out);

@@ -102,6 +102,15 @@ _SIGNATURES = {
     "abfs_part_read_depths": (ctypes.c_int, [ctypes.c_void_p, i32p]),
     "abfs_part_depths_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "abfs_part_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),
+    "abfs_part_peer_buffers": (ctypes.c_int, [ctypes.c_void_p, vpp, vpp, vpp]),
+    "abfs_part_set_peers": (ctypes.c_int, [ctypes.c_void_p, vpp, vpp, vpp, ctypes.c_uint32,
+                                           ctypes.c_uint32]),
+    "abfs_part_ipc_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "abfs_part_ipc_open": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_uint32,
+                                          ctypes.c_uint32]),
+    "abfs_part_level_p2p": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int64]),
+    "abfs_part_p2p_finish": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p, u64p]),
     "abfs_host_register": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
     "abfs_host_unregister": (ctypes.c_int, [ctypes.c_void_p]),
 }

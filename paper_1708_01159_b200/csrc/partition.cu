@@ -32,6 +32,19 @@
 
 using namespace abfs;
 
+namespace abfs {
+// Receiving side of the fused exchange: every rank adds 1 to `arrive` per
+// level (after its bitmap stores are visible system-wide) and writes its
+// level count into counts[parity][rank].
+struct PeerBox {
+    unsigned long long arrive;
+    unsigned long long pad[7];
+    unsigned long long counts[2][64];
+    unsigned long long local;      // this rank's own count (push kernel accumulator)
+    unsigned int timeout;          // set if the wait gave up
+};
+}  // namespace abfs
+
 struct abfs_part {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -56,6 +69,14 @@ struct abfs_part {
     uint64_t launches = 0;
     int last_kernel = -1;
     int last_out = 0;
+    // fused peer exchange (abfs_part_set_peers / abfs_part_ipc_open)
+    PeerBox *box = nullptr;                      // this rank's mailbox (peers write it)
+    uint32_t nranks = 0, rank = 0;
+    uint32_t **peer_fbm = nullptr;               // device [2][nranks] bitmap pointers
+    PeerBox **peer_box = nullptr;                // device [nranks] mailbox pointers
+    unsigned int *pack_ticket = nullptr;         // last-CTA ticket of the push kernel
+    unsigned long long p2p_seq = 0;              // exchanges done (every rank agrees)
+    std::vector<void *> ipc_opened;              // peer allocations mapped by IPC
 };
 
 namespace {
@@ -180,6 +201,78 @@ k_part_unpack(const uint32_t *__restrict__ gathered, Bounds b, uint64_t stride, 
         res[1] = qlen ? (unsigned long long)*qlen : *count;
 }
 
+// Fused exchange, sending side: the rank's next-frontier slice (visited bits
+// gained this level) is stored straight into EVERY rank's global
+// next-frontier bitmap over NVLink peer memory (own GPU included) -- no
+// send buffer, no collective, no unpack.  The last CTA publishes the slice
+// count into every rank's mailbox and signals arrival (system-scope atomics
+// after a system fence, so the peers see the bitmap stores first).
+__global__ void __launch_bounds__(kBlock)
+k_part_push_peers(const uint32_t *__restrict__ visited, uint32_t *vprev, uint64_t nwl,
+                  uint64_t wlo, uint32_t *const *peer_fbm, PeerBox *const *peer_box,
+                  uint32_t nranks, uint32_t rank, int parity, PeerBox *mine,
+                  unsigned int *ticket) {
+    __shared__ unsigned long long part[kWarps];
+    unsigned long long c = 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nwl;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = visited[k];
+        const uint32_t x = v & ~vprev[k];
+        vprev[k] = v;
+        for (uint32_t q = 0; q < nranks; ++q) peer_fbm[q][wlo + k] = x;
+        c += __popc(x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kWarps; ++w) s += part[w];
+        if (s) atomicAdd(&mine->local, s);
+        __threadfence_system();   // this CTA's peer stores before its ticket
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            *ticket = 0;
+            __threadfence_system();
+            const unsigned long long tot = *(volatile unsigned long long *)&mine->local;
+            mine->local = 0;
+            for (uint32_t q = 0; q < nranks; ++q)
+                *(volatile unsigned long long *)&peer_box[q]->counts[parity][rank] = tot;
+            __threadfence_system();
+            for (uint32_t q = 0; q < nranks; ++q) atomicAdd_system(&peer_box[q]->arrive, 1ull);
+        }
+    }
+}
+
+// Fused exchange, receiving side: wait until all ranks signalled this level
+// (bounded: a rank that never arrives sets `timeout` instead of hanging the
+// GPU), then sum the per-rank counts -> res = {global, this rank's}.
+__global__ void k_part_p2p_wait(PeerBox *box, unsigned long long expect, uint32_t nranks,
+                                uint32_t rank, int parity, unsigned long long *res) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long t0 = [] {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    }();
+    for (;;) {
+        if (*(volatile unsigned long long *)&box->arrive >= expect) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) {   // 20 s
+            box->timeout = 1;
+            res[0] = ~0ull;
+            return;
+        }
+        __nanosleep(200);
+    }
+    __threadfence_system();
+    unsigned long long g = 0;
+    for (uint32_t q = 0; q < nranks; ++q) g += *(volatile unsigned long long *)&box->counts[parity][q];
+    res[0] = g;
+    res[1] = *(volatile unsigned long long *)&box->counts[parity][rank];
+}
+
 }  // namespace
 
 extern "C" void abfs_part_destroy(abfs_part *p) {
@@ -190,6 +283,11 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
                    p->visited, p->vprev, p->noin, p->fnext, p->fbm[0], p->fbm[1], p->q,
                    p->qn, p->units, p->dctr, p->dmb, p->dres};
     for (void *x : dev) cudaFree(x);
+    for (void *x : p->ipc_opened) cudaIpcCloseMemHandle(x);
+    cudaFree(p->box);
+    cudaFree(p->peer_fbm);
+    cudaFree(p->peer_box);
+    cudaFree(p->pack_ticket);
     if (p->hres) cudaFreeHost(p->hres);
     if (p->e0) cudaEventDestroy(p->e0);
     if (p->e1) cudaEventDestroy(p->e1);
@@ -284,6 +382,10 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     A((void **)&p->dctr, sizeof(Ctr));
     A((void **)&p->dmb, sizeof(Mailbox));
     A((void **)&p->dres, 2 * sizeof(unsigned long long));
+    A((void **)&p->box, sizeof(PeerBox));
+    A((void **)&p->pack_ticket, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->box, 0, sizeof(PeerBox), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->pack_ticket, 0, sizeof(unsigned int), s);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&p->hres, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s);
     if (e == cudaSuccess && p->nwl) {
@@ -343,11 +445,8 @@ extern "C" int abfs_part_init(abfs_part *p, int64_t root) {
     return ABFS_OK;
 }
 
-extern "C" int abfs_part_level(abfs_part *p, int64_t level, int kernel, int variant,
-                               int64_t chunk, uint32_t *send, uint64_t stride) {
-    if (!p || !send) return fail(ABFS_EINVAL, "null argument");
+static int part_strategy(abfs_part *p, int64_t level, int kernel, int variant, int64_t chunk) {
     ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
-    if (stride < p->nwl) return fail(ABFS_EINVAL, "send stride smaller than the owned slice");
     ABFS_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = p->stream;
     ABFS_CUDA(cudaEventRecord(p->e0, s));
@@ -400,12 +499,20 @@ extern "C" int abfs_part_level(abfs_part *p, int64_t level, int kernel, int vari
     default: p->launches += launch_strategy_args<2>(c, a, kernel, chunk, s); break;
     }
     ABFS_CUDA(cudaGetLastError());
-    k_part_pack<<<grid_for(stride, kBlock, 148 * 16), kBlock, 0, s>>>(p->visited, p->vprev, p->nwl,
-                                                                      send, stride);
-    p->launches += 1;
-    ABFS_CUDA(cudaGetLastError());
     p->last_kernel = kernel;
     p->last_out = out;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_level(abfs_part *p, int64_t level, int kernel, int variant,
+                               int64_t chunk, uint32_t *send, uint64_t stride) {
+    if (!p || !send) return fail(ABFS_EINVAL, "null argument");
+    if (stride < p->nwl) return fail(ABFS_EINVAL, "send stride smaller than the owned slice");
+    ABFS_TRY(part_strategy(p, level, kernel, variant, chunk));
+    k_part_pack<<<grid_for(stride, kBlock, 148 * 16), kBlock, 0, p->stream>>>(
+        p->visited, p->vprev, p->nwl, send, stride);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
     return ABFS_OK;
 }
 
@@ -472,5 +579,139 @@ extern "C" int abfs_part_depths_device(abfs_part *p, int32_t *dev_out) {
 extern "C" int abfs_part_launches(const abfs_part *p, uint64_t *launches) {
     if (!p || !launches) return fail(ABFS_EINVAL, "null argument");
     *launches = p->launches;
+    return ABFS_OK;
+}
+
+// ---- fused peer exchange ----------------------------------------------------
+
+static int part_peers_common(abfs_part *p, uint32_t nranks, uint32_t rank,
+                             const std::vector<uint32_t *> &f0, const std::vector<uint32_t *> &f1,
+                             const std::vector<PeerBox *> &bx) {
+    ABFS_CUDA(cudaSetDevice(p->device));
+    std::vector<uint32_t *> tab(2 * (size_t)nranks);
+    for (uint32_t q = 0; q < nranks; ++q) {
+        tab[q] = f0[q];
+        tab[nranks + q] = f1[q];
+    }
+    cudaFree(p->peer_fbm);
+    cudaFree(p->peer_box);
+    p->peer_fbm = nullptr;
+    p->peer_box = nullptr;
+    ABFS_CUDA(cudaMalloc((void **)&p->peer_fbm, tab.size() * sizeof(uint32_t *)));
+    ABFS_CUDA(cudaMalloc((void **)&p->peer_box, nranks * sizeof(PeerBox *)));
+    ABFS_CUDA(cudaMemcpy(p->peer_fbm, tab.data(), tab.size() * sizeof(uint32_t *), cudaMemcpyHostToDevice));
+    ABFS_CUDA(cudaMemcpy(p->peer_box, bx.data(), nranks * sizeof(PeerBox *), cudaMemcpyHostToDevice));
+    p->nranks = nranks;
+    p->rank = rank;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_peer_buffers(abfs_part *p, void **fbm0, void **fbm1, void **mailbox) {
+    if (!p || !fbm0 || !fbm1 || !mailbox) return fail(ABFS_EINVAL, "null argument");
+    *fbm0 = p->fbm[0];
+    *fbm1 = p->fbm[1];
+    *mailbox = p->box;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_set_peers(abfs_part *p, void *const *fbm0, void *const *fbm1,
+                                   void *const *mailboxes, uint32_t nranks, uint32_t rank) {
+    if (!p || !fbm0 || !fbm1 || !mailboxes) return fail(ABFS_EINVAL, "null argument");
+    if (nranks < 1 || nranks > kMaxRanks || rank >= nranks) return fail(ABFS_EINVAL, "bad rank count");
+    if (fbm0[rank] != p->fbm[0] || fbm1[rank] != p->fbm[1] || mailboxes[rank] != p->box)
+        return fail(ABFS_EINVAL, "own buffers must sit at this rank's slot");
+    std::vector<uint32_t *> f0(nranks), f1(nranks);
+    std::vector<PeerBox *> bx(nranks);
+    for (uint32_t q = 0; q < nranks; ++q) {
+        f0[q] = (uint32_t *)fbm0[q];
+        f1[q] = (uint32_t *)fbm1[q];
+        bx[q] = (PeerBox *)mailboxes[q];
+    }
+    return part_peers_common(p, nranks, rank, f0, f1, bx);
+}
+
+extern "C" int abfs_part_ipc_export(abfs_part *p, unsigned char *handles) {
+    if (!p || !handles) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    cudaIpcMemHandle_t h[3];
+    ABFS_CUDA(cudaIpcGetMemHandle(&h[0], p->fbm[0]));
+    ABFS_CUDA(cudaIpcGetMemHandle(&h[1], p->fbm[1]));
+    ABFS_CUDA(cudaIpcGetMemHandle(&h[2], p->box));
+    std::memcpy(handles, h, sizeof(h));
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_ipc_open(abfs_part *p, const unsigned char *all_handles, uint32_t nranks,
+                                  uint32_t rank) {
+    if (!p || !all_handles) return fail(ABFS_EINVAL, "null argument");
+    if (nranks < 1 || nranks > kMaxRanks || rank >= nranks) return fail(ABFS_EINVAL, "bad rank count");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    std::vector<uint32_t *> f0(nranks), f1(nranks);
+    std::vector<PeerBox *> bx(nranks);
+    for (uint32_t q = 0; q < nranks; ++q) {
+        if (q == rank) {
+            f0[q] = p->fbm[0];
+            f1[q] = p->fbm[1];
+            bx[q] = p->box;
+            continue;
+        }
+        cudaIpcMemHandle_t h[3];
+        std::memcpy(h, all_handles + (size_t)q * 3 * sizeof(cudaIpcMemHandle_t), sizeof(h));
+        void *ptr[3];
+        for (int k = 0; k < 3; ++k) {
+            ABFS_CUDA(cudaIpcOpenMemHandle(&ptr[k], h[k], cudaIpcMemLazyEnablePeerAccess));
+            p->ipc_opened.push_back(ptr[k]);
+        }
+        f0[q] = (uint32_t *)ptr[0];
+        f1[q] = (uint32_t *)ptr[1];
+        bx[q] = (PeerBox *)ptr[2];
+    }
+    return part_peers_common(p, nranks, rank, f0, f1, bx);
+}
+
+extern "C" int abfs_part_level_p2p(abfs_part *p, int64_t level, int kernel, int variant,
+                                   int64_t chunk) {
+    if (!p) return fail(ABFS_EINVAL, "null argument");
+    if (!p->nranks) return fail(ABFS_EINVAL, "peers not set (abfs_part_set_peers / abfs_part_ipc_open)");
+    ABFS_TRY(part_strategy(p, level, kernel, variant, chunk));
+    const int parity = (int)(p->p2p_seq & 1);
+    uint32_t *const *fbm_next = p->peer_fbm + (size_t)(p->cur ^ 1) * p->nranks;
+    k_part_push_peers<<<grid_for(p->nwl, kBlock, 148 * 4), kBlock, 0, p->stream>>>(
+        p->visited, p->vprev, p->nwl, p->wlo, fbm_next, p->peer_box, p->nranks, p->rank, parity,
+        p->box, p->pack_ticket);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_p2p_finish(abfs_part *p, uint64_t *global_count, uint64_t *local_count,
+                                    uint64_t *elapsed_ns) {
+    if (!p || !global_count) return fail(ABFS_EINVAL, "null argument");
+    if (p->last_kernel < 0) return fail(ABFS_EINVAL, "finish without a level");
+    ABFS_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const int parity = (int)(p->p2p_seq & 1);
+    ++p->p2p_seq;
+    k_part_p2p_wait<<<1, 32, 0, s>>>(p->box, p->p2p_seq * p->nranks, p->nranks, p->rank, parity,
+                                     p->dres);
+    p->launches += 1;
+    ABFS_CUDA(cudaGetLastError());
+    ABFS_CUDA(cudaEventRecord(p->e1, s));
+    ABFS_CUDA(cudaMemcpyAsync(p->hres, p->dres, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    if (p->hres[0] == ~0ull)
+        return fail(ABFS_ENCCL, "peer exchange timed out (a rank never signalled this level)");
+    *global_count = p->hres[0];
+    if (local_count) *local_count = p->hres[1];
+    if (elapsed_ns) {
+        float ms = 0.f;
+        ABFS_CUDA(cudaEventElapsedTime(&ms, p->e0, p->e1));
+        const uint64_t ns = (uint64_t)((double)ms * 1e6 + 0.5);
+        *elapsed_ns = ns ? ns : 1;
+    }
+    p->cur ^= 1;
+    p->F = p->hres[0];
+    p->has_q = false;
+    p->last_kernel = -1;
     return ABFS_OK;
 }

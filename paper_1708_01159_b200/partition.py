@@ -115,6 +115,37 @@ class DevicePartition:
                 "part_exchange")
         return g.value, lc.value, ns.value
 
+    # -- fused peer exchange ---------------------------------------------------
+    def peer_buffers(self):
+        f0, f1, mb = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        L.check(L.lib().abfs_part_peer_buffers(self._h, ctypes.byref(f0), ctypes.byref(f1),
+                                               ctypes.byref(mb)), "part_peer_buffers")
+        return f0.value, f1.value, mb.value
+
+    def set_peers(self, buffers, rank: int):
+        n = len(buffers)
+        arr = [(ctypes.c_void_p * n)(*[b[k] for b in buffers]) for k in range(3)]
+        L.check(L.lib().abfs_part_set_peers(self._h, *arr, n, rank), "part_set_peers")
+
+    def ipc_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(192)
+        L.check(L.lib().abfs_part_ipc_export(self._h, buf), "part_ipc_export")
+        return buf.raw
+
+    def ipc_open(self, handles: Sequence[bytes], rank: int):
+        blob = b"".join(handles)
+        L.check(L.lib().abfs_part_ipc_open(self._h, blob, len(handles), rank), "part_ipc_open")
+
+    def level_p2p(self, level: int, kernel: int, variant: int, chunk_size: int) -> None:
+        L.check(L.lib().abfs_part_level_p2p(self._h, int(level), int(kernel), int(variant),
+                                            int(chunk_size)), "part_level_p2p")
+
+    def p2p_finish(self):
+        g, lc, ns = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        L.check(L.lib().abfs_part_p2p_finish(self._h, ctypes.byref(g), ctypes.byref(lc),
+                                             ctypes.byref(ns)), "part_p2p_finish")
+        return g.value, lc.value, ns.value
+
     def read_depths(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.owned, np.int32)
@@ -157,6 +188,43 @@ class LocalExchange:
 
     def gather_depths(self, slices: Sequence, bounds, n: int):
         return np.concatenate([s for s in slices]) if slices else np.empty(0, np.int32)
+
+
+class LocalPeerExchange(LocalExchange):
+    """Fused exchange between partitions of this process: every partition's
+    level-ending kernel stores its slice into all partitions' bitmaps."""
+
+    fused = True
+
+    def __init__(self, torch_mod, parts):
+        super().__init__(torch_mod)
+        bufs = [p.peer_buffers() for p in parts]
+        for r, p in enumerate(parts):
+            p.set_peers(bufs, r)
+
+
+class DistPeerExchange:
+    """Fused exchange, one partition per process (one GPU each): peers'
+    bitmaps and mailboxes are mapped by CUDA IPC (handles travel once over
+    torch.distributed); per level each rank's kernel stores its slice into
+    every peer's bitmap over NVLink -- no NCCL call on the data path."""
+
+    fused = True
+
+    def __init__(self, torch_mod, dist_mod, part, group=None):
+        self.torch, self.dist, self.group = torch_mod, dist_mod, group
+        self.world = dist_mod.get_world_size(group)
+        rank = dist_mod.get_rank(group)
+        handles = [None] * self.world
+        dist_mod.all_gather_object(handles, part.ipc_export(), group=group)
+        part.ipc_open(handles, rank)
+        dist_mod.barrier(group=group)
+
+    def max_over_ranks(self, x: float) -> float:
+        return DistExchange.max_over_ranks(self, x)
+
+    def gather_depths(self, slices, bounds, n: int):
+        return DistExchange.gather_depths(self, slices, bounds, n)
 
 
 class DistExchange:
@@ -209,7 +277,8 @@ class PartitionedBFS:
         self.stride = int(np.max(np.diff(self.wbounds))) if self.bounds.size > 1 else 0
         self.stride = max(self.stride, 1)
         self.exchange = exchange
-        self.sends = [alloc(self.stride) for _ in self.parts]
+        self.fused = bool(getattr(exchange, "fused", False))
+        self.sends = [] if self.fused else [alloc(self.stride) for _ in self.parts]
         self.stream = stream
         self.last_local_counts: list[list[int]] = []
         # optional: CUDA-event time of the all-gathers (bench NVLink figure)
@@ -219,6 +288,15 @@ class PartitionedBFS:
 
     # -- one level ------------------------------------------------------------
     def _level(self, level: int, kernel: int, variant: int, chunk: int):
+        if self.fused:
+            for p in self.parts:
+                p.level_p2p(level, kernel, variant, chunk)
+            res = [p.p2p_finish() for p in self.parts]
+            counts = {r[0] for r in res}
+            if len(counts) != 1:
+                raise RuntimeError(f"partitions disagree on the level count: {sorted(counts)}")
+            self.last_local_counts.append([r[1] for r in res])
+            return res[0][0], max(r[2] for r in res)
         for p, s in zip(self.parts, self.sends):
             p.level(level, kernel, variant, chunk, s)
         if self.time_exchange:
@@ -307,4 +385,5 @@ def local_partitions(dgraph, parts: int, stream_ptr: int | None = None):
 
 
 __all__ = ["ALIGN", "edge_balanced_bounds", "word_bounds", "DevicePartition", "LocalExchange",
-           "DistExchange", "PartitionedBFS", "local_partitions"]
+           "LocalPeerExchange", "DistExchange", "DistPeerExchange", "PartitionedBFS",
+           "local_partitions"]

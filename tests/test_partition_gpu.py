@@ -17,7 +17,8 @@ import paper_1708_01159_b200 as P
 from paper_1708_01159_b200 import DeviceGraph, Traversal
 from paper_1708_01159_b200.features import static_vector
 from paper_1708_01159_b200.graph import stats_from_offsets
-from paper_1708_01159_b200.partition import LocalExchange, PartitionedBFS, local_partitions
+from paper_1708_01159_b200.partition import (LocalExchange, LocalPeerExchange, PartitionedBFS,
+                                             local_partitions)
 
 pytestmark = pytest.mark.gpu
 
@@ -25,21 +26,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MODEL = os.path.join(ROOT, "models", "gpu_tree.tree")
 
 
-def make_bfs(dg, parts):
+def make_bfs(dg, parts, exchange="gather"):
+    """exchange: "gather" = send buffers + all-gather (device concat here, NCCL
+    across GPUs); "peer" = fused kernel stores into every partition's bitmap."""
     stream = torch.cuda.current_stream().cuda_stream
     ps, bounds = local_partitions(dg, parts, stream)
-    return PartitionedBFS(ps, bounds, LocalExchange(torch),
+    ex = LocalExchange(torch) if exchange == "gather" else LocalPeerExchange(torch, ps)
+    return PartitionedBFS(ps, bounds, ex,
                           alloc=lambda s: torch.zeros(s, dtype=torch.int32, device="cuda"))
 
 
+@pytest.mark.parametrize("exchange", ["gather", "peer"])
 @pytest.mark.parametrize("parts", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", ["kron10", "kron12", "u1000", "er12", "mesh64", "hand1",
                                   "unreach", "dup", "selfloop", "star7", "single", "path9"])
-def test_partitions_all_pairs_match_golden(name, parts):
+def test_partitions_all_pairs_match_golden(name, parts, exchange):
     n, m, a = G.graph_arrays(name)
     g = P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS])
     dg = DeviceGraph.upload(g)
-    bfs = make_bfs(dg, parts)
+    bfs = make_bfs(dg, parts, exchange)
     stats = stats_from_offsets(n, m, a["out_offsets"], a["in_offsets"])
     traces = G.traces()["small"]
     for r in G.roots(name):
@@ -58,8 +63,9 @@ def test_partitions_all_pairs_match_golden(name, parts):
             np.testing.assert_array_equal(bfs.depths(), want)
 
 
+@pytest.mark.parametrize("exchange", ["gather", "peer"])
 @pytest.mark.parametrize("cfg,parts", [("k18", 8), ("er18", 4), ("mesh256", 3)])
-def test_partitions_equal_single_gpu_engine(cfg, parts):
+def test_partitions_equal_single_gpu_engine(cfg, parts, exchange):
     if cfg.startswith("k"):
         dg = DeviceGraph.rmat(18, 16 << 18, 1, symmetrize=True)
     elif cfg.startswith("er"):
@@ -69,7 +75,7 @@ def test_partitions_equal_single_gpu_engine(cfg, parts):
     stats = P.compute_stats(dg)
     flat = P.deserialize(MODEL)
     t = Traversal(dg)
-    bfs = make_bfs(dg, parts)
+    bfs = make_bfs(dg, parts, exchange)
     oo, _ = dg.offsets()
     cand = np.flatnonzero(np.diff(oo.astype(np.int64)) > 0)
     for r in [int(cand[0]), int(cand[len(cand) // 2]), int(cand[-1])]:
@@ -95,3 +101,15 @@ def test_partition_rejects_misaligned_range():
         DevicePartition(dg, 5, 64)
     with pytest.raises(ValueError, match="out of bounds"):
         DevicePartition(dg, 0, n + 1)
+
+
+def test_peer_exchange_over_cuda_ipc_two_processes():
+    """DistPeerExchange: two processes (one GPU here; one per GPU in
+    production) map each other's bitmaps/mailboxes by CUDA IPC and exchange
+    frontier slices with the fused peer-store kernel."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from tools import ipc_two_ranks
+    for rank, status, checked in ipc_two_ranks.main():
+        assert status == "ok", f"rank {rank}:\n{status}"
+        assert checked > 0
