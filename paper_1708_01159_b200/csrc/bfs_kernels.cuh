@@ -581,6 +581,7 @@ template <int VAR>
 __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ in_off,
                                           const uint32_t *__restrict__ src,
+                                          const uint32_t *__restrict__ first_src,
                                           const uint32_t *__restrict__ noin,
                                           uint32_t *__restrict__ fbm_next, uint64_t word0,
                                           uint64_t words, uint32_t *wbuf, uint32_t *wfound) {
@@ -630,15 +631,29 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             for (uint32_t base = 0; base < total; base += 32) {
                 const bool has = base + lane < total;
                 const uint32_t v = has ? wbuf[base + lane] : 0u;
-                uint32_t j = 0, e = 0;
+                uint32_t j = 0, e = 0, f0 = 0;
                 if (has) {
+                    // the offsets and the first in-neighbour (dense array,
+                    // coalesced over consecutive candidates) load together
                     j = __ldg(in_off + v);
                     e = __ldg(in_off + v + 1);
+                    f0 = __ldg(first_src + v);
                 }
-                // phase A: each candidate scans up to pull_light of its own
-                // in-neighbours one aligned 16-byte load per step (one L1
-                // wavefront per lane instead of four), early exit
+                // probe 0: the smallest in-neighbour (a hub on skewed graphs,
+                // so most candidates stop here without touching src)
                 bool found = false;
+                if (j < e) {
+                    ++scanned;
+                    if (in_bitmap(c.fbm, f0)) {
+                        found = true;
+                        j = e;
+                    } else {
+                        ++j;
+                    }
+                }
+                // phase A: each candidate scans up to pull_light more of its
+                // in-neighbours, one aligned 16-byte load per step (one L1
+                // wavefront per lane instead of four), early exit
                 const uint32_t ja = min(e, j + c.pull_light);
                 while (__any_sync(kFull, j < ja)) {
                     if (j < ja) {
@@ -738,13 +753,14 @@ struct SmemPull {
 template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
-       const uint32_t *__restrict__ noin, uint32_t *__restrict__ fbm_next, uint64_t word0,
-       uint64_t words) {
+       const uint32_t *__restrict__ first_src, const uint32_t *__restrict__ noin,
+       uint32_t *__restrict__ fbm_next, uint64_t word0, uint64_t words) {
     __shared__ unsigned int sn;
     __shared__ SmemPull sp;
     zero_slot(c);
     const unsigned w = threadIdx.x >> 5;
-    pull_body<VAR>(c, &sn, in_off, src, noin, fbm_next, word0, words, sp.list[w], sp.found[w]);
+    pull_body<VAR>(c, &sn, in_off, src, first_src, noin, fbm_next, word0, words, sp.list[w],
+                   sp.found[w]);
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit

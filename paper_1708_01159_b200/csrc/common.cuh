@@ -45,6 +45,8 @@ struct DevGraph {
     uint32_t *in_off = nullptr;    // [n+1]
     uint32_t *src = nullptr;       // [m] sources, sorted by (dest, origin)
     uint32_t *rev_owner = nullptr; // [m] owning destination of reverse slot
+    uint32_t *first_src = nullptr; // [n] src[in_off[v]]: pull's first probe as a dense,
+                                   //     coalesced read (derived, like rev_owner)
 };
 
 }  // namespace abfs

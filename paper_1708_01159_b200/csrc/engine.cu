@@ -108,6 +108,7 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
     a.src = g.src;
     a.rev_owner = g.rev_owner;
     a.m_rev = g.m;
+    a.first_src = g.first_src;
     a.noin = t->noin;
     a.fbm_next = t->fbm[t->cur ^ 1];
     a.word0 = 0;
@@ -560,6 +561,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.in_off = g.in_off;
     P.src = g.src;
     P.rev_owner = g.rev_owner;
+    P.first_src = g.first_src;
     P.n = g.n;
     P.m = g.m;
     P.words = t->words;

@@ -255,7 +255,21 @@ int new_graph(int device, uint64_t n, uint64_t m, abfs_graph **out) {
     return ABFS_OK;
 }
 
+__global__ void k_first_src(const uint32_t *__restrict__ in_off, const uint32_t *__restrict__ src,
+                            uint64_t n, uint32_t *first_src) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = in_off[v], e = in_off[v + 1];
+        first_src[v] = b < e ? src[b] : 0u;
+    }
+}
+
 int finish_build(int rc, abfs_graph *g, abfs_graph **out) {
+    if (rc == ABFS_OK && g->d.n) {
+        k_first_src<<<grid_cap(g->d.n, 256), 256>>>(g->d.in_off, g->d.src, g->d.n, g->d.first_src);
+        const cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("first_src: ") + cudaGetErrorString(e));
+    }
     if (rc != ABFS_OK) {
         abfs_graph_destroy(g);
         *out = nullptr;
@@ -282,6 +296,7 @@ int graph_alloc(abfs_graph *g, uint64_t n, uint64_t m) {
     A(&d.org, mb);
     A(&d.src, mb);
     A(&d.rev_owner, mb);
+    A(&d.first_src, (n ? n : 1) * 4 + 16);
     if (e != cudaSuccess) {
         graph_free(g);
         return fail(e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA,
@@ -298,6 +313,7 @@ void graph_free(abfs_graph *g) {
     cudaFree(d.org);
     cudaFree(d.src);
     cudaFree(d.rev_owner);
+    cudaFree(d.first_src);
     d = DevGraph();
 }
 

@@ -49,6 +49,7 @@ struct StratArgs {
     // reverse slots (sorted by owner): in-CSR + owners, m_rev slots
     const uint32_t *in_off, *src, *rev_owner;
     uint64_t m_rev;
+    const uint32_t *first_src;   // src[in_off[v]] by global id
     // pull: in-degree-0 bitmap, next-frontier bitmap, word range scanned
     const uint32_t *noin;
     uint32_t *fbm_next;
@@ -77,7 +78,7 @@ static int launch_strategy_args(const LevelCtx &c, const StratArgs &a, int kerne
         return 2;
     case ABFS_VERTEX_PULL:
         k_pull<VAR><<<grid_for(a.word_end - a.word0, kBlock, 148 * 64), kBlock, 0, s>>>(
-            c, a.in_off, a.src, a.noin, a.fbm_next, a.word0, a.word_end);
+            c, a.in_off, a.src, a.first_src, a.noin, a.fbm_next, a.word0, a.word_end);
         k_pull_heavy<<<148 * 8, kBlock, 0, s>>>(c, a.in_off, a.src, a.fbm_next);
         return 2;
     default: {  // VERTEX_PUSH_WARP: nearest legal virtual-warp width <= chunk

@@ -36,7 +36,7 @@ struct MegaParams {
     uint32_t *q0, *q1;
     uint2 *units;
     Ctr *ctr;
-    const uint32_t *out_off, *dst, *org, *in_off, *src, *rev_owner;
+    const uint32_t *out_off, *dst, *org, *in_off, *src, *rev_owner, *first_src;
     uint64_t n, m, words;
     // tree blob (FlatTree arrays + the 24 static features), device copy;
     // sel points at its start, o_* are byte offsets within it
@@ -126,7 +126,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
             // the pull scratch lists alias the (idle) CTA queue buffer
             static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");
             const unsigned w = threadIdx.x >> 5;
-            pull_body<VAR>(c, sn, P.in_off, P.src, P.noin, fbm_next, 0, P.words,
+            pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, 0, P.words,
                            sq->buf + w * kPullList, pfound + w * kPullSub);
         }
         grid.sync();

@@ -52,6 +52,7 @@ struct abfs_part {
     uint64_t n = 0, lo = 0, hi = 0, wlo = 0, whi = 0, W = 0, nv = 0, nwl = 0, mf = 0, mr = 0;
     uint32_t *fo_off = nullptr, *fo_dst = nullptr, *fo_org = nullptr;   // filtered forward
     uint32_t *r_off = nullptr, *r_src = nullptr, *r_own = nullptr;      // owned reverse rows
+    uint32_t *r_first = nullptr;                                         // first_src[lo, hi)
     int32_t *depth = nullptr;                                            // [nv]
     uint32_t *visited = nullptr, *vprev = nullptr, *noin = nullptr, *fnext = nullptr;  // [nwl]
     uint32_t *fbm[2] = {nullptr, nullptr};                               // global [W]
@@ -279,7 +280,7 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
     if (!p) return;
     cudaSetDevice(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
-    void *dev[] = {p->fo_off, p->fo_dst, p->fo_org, p->r_off, p->r_src, p->r_own, p->depth,
+    void *dev[] = {p->fo_off, p->fo_dst, p->fo_org, p->r_off, p->r_src, p->r_own, p->r_first, p->depth,
                    p->visited, p->vprev, p->noin, p->fnext, p->fbm[0], p->fbm[1], p->q,
                    p->qn, p->units, p->dctr, p->dmb, p->dres};
     for (void *x : dev) cudaFree(x);
@@ -357,6 +358,9 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     A((void **)&p->r_off, (p->nv + 1) * 4);
     A((void **)&p->r_src, p->mr * 4 + 16);   // +16: aligned 16-byte reads in pull
     A((void **)&p->r_own, p->mr * 4);
+    A((void **)&p->r_first, p->nv * 4 + 16);
+    if (e == cudaSuccess && p->nv)
+        e = cudaMemcpyAsync(p->r_first, g->d.first_src + lo, p->nv * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && p->mr)
         e = cudaMemcpyAsync(p->r_src, g->d.src + rb, p->mr * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && p->mr)
@@ -487,6 +491,7 @@ static int part_strategy(abfs_part *p, int64_t level, int kernel, int variant, i
     a.src = p->r_src;
     a.rev_owner = p->r_own;
     a.m_rev = p->mr;
+    a.first_src = p->r_first - p->lo;
     a.noin = p->noin - p->wlo;
     a.fbm_next = p->fnext - p->wlo;
     a.word0 = p->wlo;
