@@ -576,6 +576,8 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // ---------------------------------------------------------------------------
 constexpr int kPullSub = 8;                  // words per sub-tile
 constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
+constexpr int kPullChunkSubs = 8;            // sub-tiles per CTA chunk fetch
+constexpr uint32_t kFetchInit = 0xfffffffeu, kFetchDone = 0xffffffffu;
 
 template <int VAR>
 __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
@@ -584,22 +586,53 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ first_src,
                                           const uint32_t *__restrict__ noin,
                                           uint32_t *__restrict__ fbm_next, uint64_t word0,
-                                          uint64_t words, uint32_t *wbuf, uint32_t *wfound) {
+                                          uint64_t words, uint32_t *wbuf, uint32_t *wfound,
+                                          unsigned long long *sfetch) {
     // words [word0, words) of the bitmaps (a vertex partition passes its
     // owned range; bitmap/offset pointers are indexed by global ids);
     // wbuf = kPullList entries, wfound = kPullSub words, both per warp
+    // Work distribution: the CTA fetches chunks of kPullChunkSubs sub-tiles
+    // with one global atomic; its warps take single sub-tiles from the
+    // chunk through a shared-memory cursor (packed chunk id : next index).
+    // The warp that overflows the cursor refills it; the others wait for the
+    // new chunk id.  Few global atomics (sparse levels stay cheap) and an
+    // 8-word grain at the end of the level (dense levels balance).
     CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
-    const uint64_t ntiles = (words - word0 + 31) / 32;
+    const uint64_t nsub = (words - word0 + kPullSub - 1) / kPullSub;
+    const uint64_t nchunks = (nsub + kPullChunkSubs - 1) / kPullChunkSubs;
+    if (threadIdx.x == 0) *sfetch = ((unsigned long long)kFetchInit << 32) | kPullChunkSubs;
+    __syncthreads();
     unsigned long long scanned = 0;
     for (;;) {
-        unsigned long long tile = 0;
-        if (lane == 0) tile = atomicAdd(c.work, 1ull);
-        tile = __shfl_sync(kFull, tile, 0);
-        if (tile >= ntiles) break;
-        for (int sub = 0; sub < 32 / kPullSub; ++sub) {
-            const uint64_t wbase = word0 + tile * 32 + (uint64_t)sub * kPullSub;
-            if (wbase >= words) break;
+        unsigned long long st = 0;
+        if (lane == 0) st = atomicAdd(sfetch, 1ull);
+        st = __shfl_sync(kFull, st, 0);
+        uint32_t cid = (uint32_t)(st >> 32), sidx = (uint32_t)st;
+        if (cid == kFetchDone) break;
+        if (sidx > (uint32_t)kPullChunkSubs) {   // another warp is refilling the chunk
+            if (lane == 0)
+                while ((uint32_t)(*(volatile unsigned long long *)sfetch >> 32) == cid) {
+                }
+            __syncwarp();
+            continue;
+        }
+        if (sidx == (uint32_t)kPullChunkSubs) {  // this warp refills it
+            unsigned long long g = 0;
+            if (lane == 0) {
+                g = atomicAdd(c.work, 1ull);
+                atomicExch(sfetch, g < nchunks ? (g << 32) | 1ull
+                                               : (unsigned long long)kFetchDone << 32);
+            }
+            g = __shfl_sync(kFull, g, 0);
+            if (g >= nchunks) break;
+            cid = (uint32_t)g;
+            sidx = 0;
+        }
+        const uint64_t sg = (uint64_t)cid * kPullChunkSubs + sidx;
+        if (sg >= nsub) continue;
+        {
+            const uint64_t wbase = word0 + sg * kPullSub;
             const uint64_t myw = wbase + lane;
             const bool mine = lane < (unsigned)kPullSub && myw < words;
             uint32_t vis = 0xffffffffu, cand = 0;
@@ -757,10 +790,11 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
        uint32_t *__restrict__ fbm_next, uint64_t word0, uint64_t words) {
     __shared__ unsigned int sn;
     __shared__ SmemPull sp;
+    __shared__ unsigned long long sfetch;
     zero_slot(c);
     const unsigned w = threadIdx.x >> 5;
     pull_body<VAR>(c, &sn, in_off, src, first_src, noin, fbm_next, word0, words, sp.list[w],
-                   sp.found[w]);
+                   sp.found[w], &sfetch);
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit

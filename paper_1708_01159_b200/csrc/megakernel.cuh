@@ -102,7 +102,8 @@ template <int VAR>
 __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
                                               uint32_t F, const uint32_t *q, uint32_t *fbm_next,
                                               SmemQ *sq, unsigned *sn, int *s_done,
-                                              uint32_t *pfound, cg::grid_group &grid) {
+                                              uint32_t *pfound, unsigned long long *sfetch,
+                                              cg::grid_group &grid) {
     // Two-phase strategies (light pass, then CTA work units) need a second
     // barrier only if the light pass created units: after the first barrier
     // every CTA reads the same unit count, and with none the level's count
@@ -127,7 +128,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
             static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");
             const unsigned w = threadIdx.x >> 5;
             pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, 0, P.words,
-                           sq->buf + w * kPullList, pfound + w * kPullSub);
+                           sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
         }
         grid.sync();
         if (!units()) return;
@@ -149,6 +150,7 @@ template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
     __shared__ uint32_t pfound[kWarps * kPullSub];
+    __shared__ unsigned long long s_fetch;
     __shared__ unsigned sn;
     __shared__ int s_done;
     __shared__ int s_cls;
@@ -279,9 +281,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
         switch (pv) {
-        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
-        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
-        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, grid); break;
+        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
         }
         const bool topdown = pk != 3;
         const unsigned long long nw = topdown
