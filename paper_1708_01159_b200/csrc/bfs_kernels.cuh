@@ -423,7 +423,8 @@ __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
             if (e - j > kPushHub) {
                 const uint32_t nu = (e - j + kUnit - 1) / kUnit;
                 const uint32_t s = atomicAdd(c.units_tail, nu);
-                for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(u, k);
+                for (uint32_t k = 0; k < nu; ++k)
+                    c.units[s + k] = make_uint2(j + k * kUnit, min(e, j + (k + 1) * kUnit));
                 j = e;
             }
         }
@@ -484,7 +485,8 @@ __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
                 if (sl == 0) {
                     const uint32_t nu = (en - b + kUnit - 1) / kUnit;
                     const uint32_t s = atomicAdd(c.units_tail, nu);
-                    for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(u, k);
+                    for (uint32_t k = 0; k < nu; ++k)
+                        c.units[s + k] = make_uint2(b + k * kUnit, min(en, b + (k + 1) * kUnit));
                 }
             } else {
                 j = b + sl;
@@ -525,10 +527,13 @@ __device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
     QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     const unsigned nunits = *(volatile unsigned *)c.units_tail;
+    // push units carry their adjacency slice [x, y) directly (no offset
+    // lookup); the next unit's descriptor is loaded while this one runs
+    uint2 nxt = blockIdx.x < nunits ? c.units[blockIdx.x] : make_uint2(0, 0);
     for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
-        const uint2 un = c.units[w];
-        const uint32_t b = __ldg(out_off + un.x) + un.y * kUnit;
-        const uint32_t e = min(__ldg(out_off + un.x + 1), b + kUnit);
+        const uint2 un = nxt;
+        if (w + gridDim.x < nunits) nxt = c.units[w + gridDim.x];
+        const uint32_t b = un.x, e = un.y;
         for (uint32_t jb = b; jb < e; jb += kBlock * 4) {
             uint32_t v[4];
             bool act[4], won[4];
