@@ -465,11 +465,43 @@ static int finish_traversal(abfs_traversal *t, size_t n_levels, int32_t *depths_
 
 constexpr uint32_t kMegaCap = 1u << 16;   // level records kept by the megakernel
 
-static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-
 // Run a whole traversal in the persistent cooperative kernel.  fixed_pair
 // >= 0 runs bfs_full with that pair; otherwise the tree picks per level.
 constexpr size_t kMaxBatch = 4096;         // roots per batched megakernel launch
+
+// The tree with every node that tests a STATIC feature (vertex / edge count,
+// degree summaries) resolved for this graph: those comparisons have the same
+// outcome at every level, so the device walk only visits nodes on the four
+// per-level features.  Leaf reached for any feature vector is unchanged.
+struct PrunedTree {
+    std::vector<uint16_t> feat;
+    std::vector<double> thr;
+    std::vector<uint32_t> left, right;
+    std::vector<uint8_t> cls;
+};
+
+static bool dynamic_feature(int canon) { return canon >= 2 && canon <= 5; }
+
+static uint32_t prune_node(const abfs_tree *tr, const double *st, uint32_t node, PrunedTree &out) {
+    while (tr->leaf_classes[node] == ABFS_NOT_A_LEAF) {
+        const int canon = tr->selection[tr->features[node]];
+        if (dynamic_feature(canon)) break;
+        node = (st[canon] < tr->thresholds[node]) ? tr->lefts[node] : tr->rights[node];
+    }
+    const uint32_t idx = (uint32_t)out.cls.size();
+    out.feat.push_back(tr->features[node]);
+    out.thr.push_back(tr->thresholds[node]);
+    out.left.push_back(0);
+    out.right.push_back(0);
+    out.cls.push_back(tr->leaf_classes[node]);
+    if (tr->leaf_classes[node] == ABFS_NOT_A_LEAF) {
+        const uint32_t l = prune_node(tr, st, tr->lefts[node], out);
+        const uint32_t r = prune_node(tr, st, tr->rights[node], out);
+        out.left[idx] = l;
+        out.right[idx] = r;
+    }
+    return idx;
+}
 
 // roots: nroots >= 1 traversals run back to back in one launch; with
 // host_init the host ran init_depths for the single root, otherwise every
@@ -502,12 +534,12 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
         t->mega_grid = per * sms;
     }
-    // stage tree + static features (small) into one device blob
-    const uint32_t nn = tr ? tr->node_count : 0, ns = tr ? tr->n_selection : 0;
-    const size_t o_sel = 0, o_feat = align16(o_sel + ns * 2), o_thr = align16(o_feat + nn * 2);
-    const size_t o_left = align16(o_thr + nn * 8), o_right = align16(o_left + nn * 4);
-    const size_t o_cls = align16(o_right + nn * 4), o_st = align16(o_cls + nn);
-    const size_t bytes = align16(o_st + 24 * 8);
+    // stage the device tree: static-feature nodes resolved, float64 tests on
+    // the per-level features turned into exact integer cutoffs (CutNode)
+    PrunedTree pt;
+    if (tr && static24) prune_node(tr, static24, 0, pt);
+    const uint32_t nn = (uint32_t)pt.cls.size();
+    const size_t bytes = (nn ? nn : 1) * sizeof(CutNode);
     if (bytes > t->tree_cap) {
         cudaFree(t->dtree);
         if (t->htree) cudaFreeHost(t->htree);
@@ -519,15 +551,32 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         t->tree_cap = bytes * 2;
     }
     std::vector<unsigned char> blob(bytes, 0);
-    if (tr) {
-        std::memcpy(blob.data() + o_sel, tr->selection, ns * 2);
-        std::memcpy(blob.data() + o_feat, tr->features, nn * 2);
-        std::memcpy(blob.data() + o_thr, tr->thresholds, nn * 8);
-        std::memcpy(blob.data() + o_left, tr->lefts, nn * 4);
-        std::memcpy(blob.data() + o_right, tr->rights, nn * 4);
-        std::memcpy(blob.data() + o_cls, tr->leaf_classes, nn);
+    if (nn) {
+        const uint64_t n = g.n;
+        const double nv = (double)(unsigned long long)static24[0];
+        CutNode *cn = reinterpret_cast<CutNode *>(blob.data());
+        for (uint32_t k = 0; k < nn; ++k) {
+            cn[k].cls = pt.cls[k];
+            cn[k].left = pt.left[k];
+            cn[k].right = pt.right[k];
+            if (pt.cls[k] != ABFS_NOT_A_LEAF) continue;
+            const int canon = tr->selection[pt.feat[k]];
+            const double thr = pt.thr[k];
+            const bool pct = canon == 3 || canon == 5;
+            cn[k].on_disc = (canon == 4 || canon == 5) ? 1 : 0;
+            // smallest k in [0, n] failing "x(k) < thr" (n + 1 if none does)
+            auto holds = [&](uint64_t x) {
+                return pct ? ((double)x / nv < thr) : ((double)x < thr);
+            };
+            uint64_t lo = 0, hi = n + 1;
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                if (holds(mid)) lo = mid + 1;
+                else hi = mid;
+            }
+            cn[k].cutoff = lo;
+        }
     }
-    if (static24) std::memcpy(blob.data() + o_st, static24, 24 * 8);
     if (blob != t->last_blob) {
         // every mega_run ends with a stream sync, so the pinned staging copy
         // is never in flight here; an unchanged tree is not re-uploaded
@@ -565,15 +614,8 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.n = g.n;
     P.m = g.m;
     P.words = t->words;
-    P.sel = (const uint16_t *)t->dtree;
-    P.tree_bytes = (uint32_t)bytes;
-    P.o_sel = (uint32_t)o_sel;
-    P.o_feat = (uint32_t)o_feat;
-    P.o_thr = (uint32_t)o_thr;
-    P.o_left = (uint32_t)o_left;
-    P.o_right = (uint32_t)o_right;
-    P.o_cls = (uint32_t)o_cls;
-    P.o_st = (uint32_t)o_st;
+    P.tree = t->dtree;
+    P.tree_nodes = nn;
     P.fixed_pair = fixed_pair;
     P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
     P.instrument = t->instrument ? 1 : 0;

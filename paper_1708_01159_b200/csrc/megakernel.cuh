@@ -38,10 +38,9 @@ struct MegaParams {
     Ctr *ctr;
     const uint32_t *out_off, *dst, *org, *in_off, *src, *rev_owner, *first_src;
     uint64_t n, m, words;
-    // tree blob (FlatTree arrays + the 24 static features), device copy;
-    // sel points at its start, o_* are byte offsets within it
-    const uint16_t *sel;
-    uint32_t tree_bytes, o_sel, o_feat, o_thr, o_left, o_right, o_cls, o_st;
+    // device tree: CutNode array (see below), staged into shared memory
+    const void *tree;
+    uint32_t tree_nodes;
     int fixed_pair;      // >= 0: bfs_full with this pair ordinal, no tree
     int vw_log2;
     int instrument;
@@ -64,38 +63,36 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// The FlatTree and the static features live in shared memory for the whole
-// traversal (grid barriers flush L1, so global reads would cost an L2 round
-// trip per node per level).
-constexpr uint32_t kMegaTreeSmem = 16384;   // bytes: trees up to ~800 nodes
-
-struct SmemTree {
-    const uint16_t *sel, *feat;
-    const double *thr, *st;
-    const uint32_t *left, *right;
-    const uint8_t *cls;
+// The tree as the device walks it.  The host (engine.cu, mega_run) resolves
+// every node on a static feature for this graph and turns each remaining
+// float64 test on a per-level feature into an exact integer cutoff:
+//   frontier_abs / discovered_abs:  (double)k < thr
+//   frontier_pct / discovered_pct:  (double)k / (double)|V| < thr
+// are monotone in the integer k (IEEE conversion and division are correctly
+// rounded), so each is "k < cutoff" with cutoff = the smallest k failing the
+// test, found on the host with the very same float64 arithmetic.  The walk is
+// then integer compares on shared memory: same leaf as tree.py:332-339 for
+// every reachable (frontier, discovered).
+struct CutNode {
+    unsigned long long cutoff;
+    uint32_t left, right;
+    uint8_t cls;       // 255 = internal
+    uint8_t on_disc;   // 0: compare frontier, 1: compare discovered
+    uint8_t pad[14];
 };
+static_assert(sizeof(CutNode) == 32, "CutNode layout");
 
-__device__ __forceinline__ int mega_tree_class(const SmemTree &T, unsigned long long frontier,
+constexpr uint32_t kMegaTreeNodes = 512;   // 16 KB of shared memory
+
+__device__ __forceinline__ int mega_tree_class(const CutNode *T, unsigned long long frontier,
                                                unsigned long long discovered) {
-    // extract_runtime_features (features.py:98-121) + FlatTree.predict_one
-    // (tree.py:332-339): float64 true division, strict < goes left.
-    const double nd = T.st[0];
-    const unsigned long long nv = (unsigned long long)nd;
     uint32_t node = 0;
-    while (T.cls[node] == 255) {
-        const int canon = T.sel[T.feat[node]];
-        double x;
-        switch (canon) {
-        case 2: x = (double)frontier; break;
-        case 3: x = (double)frontier / (double)nv; break;
-        case 4: x = (double)discovered; break;
-        case 5: x = (double)discovered / (double)nv; break;
-        default: x = T.st[canon];
-        }
-        node = (x < T.thr[node]) ? T.left[node] : T.right[node];
+    while (T[node].cls == 255) {
+        const CutNode &n = T[node];
+        const unsigned long long x = n.on_disc ? discovered : frontier;
+        node = x < n.cutoff ? n.left : n.right;
     }
-    return T.cls[node];
+    return T[node].cls;
 }
 
 template <int VAR>
@@ -156,27 +153,19 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ int s_cls;
     __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned s_base;
-    __shared__ __align__(16) unsigned char s_tree[kMegaTreeSmem];
+    __shared__ __align__(16) CutNode s_tree[kMegaTreeNodes];
     cg::grid_group grid = cg::this_grid();
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-    // stage the tree blob (same layout as the device copy) into shared memory
-    SmemTree T;
-    {
-        const unsigned char *src_blob = reinterpret_cast<const unsigned char *>(P.sel);
-        const bool fits = P.tree_bytes <= kMegaTreeSmem;
-        const unsigned char *base = fits ? s_tree : src_blob;
-        if (fits)
-            for (uint32_t i = threadIdx.x * 16; i < P.tree_bytes; i += kBlock * 16)
-                *reinterpret_cast<uint4 *>(s_tree + i) = *reinterpret_cast<const uint4 *>(src_blob + i);
-        __syncthreads();
-        T.sel = reinterpret_cast<const uint16_t *>(base + P.o_sel);
-        T.feat = reinterpret_cast<const uint16_t *>(base + P.o_feat);
-        T.thr = reinterpret_cast<const double *>(base + P.o_thr);
-        T.left = reinterpret_cast<const uint32_t *>(base + P.o_left);
-        T.right = reinterpret_cast<const uint32_t *>(base + P.o_right);
-        T.cls = base + P.o_cls;
-        T.st = reinterpret_cast<const double *>(base + P.o_st);
+    // stage the tree into shared memory (global fallback if it is too big)
+    const CutNode *T = reinterpret_cast<const CutNode *>(P.tree);
+    if (P.tree_nodes <= kMegaTreeNodes) {
+        const uint4 *src4 = reinterpret_cast<const uint4 *>(P.tree);
+        uint4 *dst4 = reinterpret_cast<uint4 *>(s_tree);
+        for (uint32_t i = threadIdx.x; i < P.tree_nodes * 2; i += kBlock)
+            dst4[i] = src4[i];
+        T = s_tree;
     }
+    __syncthreads();
     unsigned long long rec_off = 0;
     for (uint32_t ri = 0; ri < P.nroots; ++ri) {
     if (P.init_in_kernel) {
@@ -289,7 +278,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         const unsigned long long nw = topdown
             ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
             : *(volatile unsigned long long *)&P.ctr->count[out];
+#ifdef ABFS_NO_RECORDS   // overhead experiment only
+        if (false) {
+#else
         if (lead && rec_off + level < P.cap) {
+#endif
             MegaRecord &r = P.recs[rec_off + level];
             r.kernel = pk;
             r.variant = pv;
