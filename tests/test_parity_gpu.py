@@ -246,3 +246,69 @@ def test_adaptive_batch_matches_single_traversals(name):
     with pytest.raises(ValueError, match="out of range"):
         t.adaptive_batch([0, g.vertex_count], flat.as_abfs(), static_vector(stats))
     t.close()
+
+
+def _random_tree(rng, selection, values, depth):
+    """Preorder FlatTree of the given depth; thresholds drawn from the exact
+    feature values a traversal produces and their float64 neighbours (the
+    boundary cases of `x < thr`), leaves random pairs or UNKNOWN."""
+    feats, thrs, lefts, rights, cls = [], [], [], [], []
+
+    def node(d):
+        i = len(cls)
+        feats.append(0), thrs.append(0.0), lefts.append(0), rights.append(0), cls.append(255)
+        if d == depth or rng.random() < 0.15:
+            cls[i] = int(rng.choice([*range(15), 254]))
+            return i
+        f = int(rng.integers(len(selection)))
+        base = float(rng.choice(values[selection[f]]))
+        feats[i] = f
+        thrs[i] = float(rng.choice([base, np.nextafter(base, np.inf), np.nextafter(base, -np.inf)]))
+        lefts[i] = node(d + 1)
+        rights[i] = node(d + 1)
+        return i
+
+    node(0)
+    return P.FlatTree(tuple(selection), np.array(feats, np.uint16), np.array(thrs, np.float64),
+                      np.array(lefts, np.uint32), np.array(rights, np.uint32),
+                      np.array(cls, np.uint8))
+
+
+@pytest.mark.parametrize("name", ["mesh64", "kron12", "u1000"])
+def test_device_tree_cutoffs_match_float64_walk(name):
+    """The megakernel walks an integer-cutoff form of the tree (static nodes
+    resolved per graph, float64 tests on frontier/discovered turned into
+    exact integer cutoffs); its traces must equal the launch path's float64
+    walk for random trees whose thresholds sit exactly on, and one ulp around,
+    the feature values the traversal produces."""
+    g = graph(name)
+    t = g.device_graph().scratch()
+    stats = P.compute_stats(g)
+    r = G.roots(name)[0]
+    cnt = G.counts(name, r).tolist()
+    fr = [1] + cnt[:-1]
+    disc = list(np.cumsum([1] + cnt[:-1]))
+    n = g.vertex_count
+    from paper_1708_01159_b200.features import FEATURE_NAMES
+    fv = P.extract_runtime_features(stats, 1, 1)
+    values = {nm: [fv.scalar(nm)] for nm in FEATURE_NAMES}
+    values["frontier_abs"] = [float(x) for x in fr]
+    values["frontier_pct"] = [x / n for x in fr]
+    values["discovered_abs"] = [float(x) for x in disc]
+    values["discovered_pct"] = [x / n for x in disc]
+    rng = np.random.default_rng(7)
+    sel = ["vertex_count", "frontier_abs", "frontier_pct", "discovered_abs", "discovered_pct",
+           "out_deg.median", "edge_count"]
+    try:
+        for _ in range(12):
+            flat = _random_tree(rng, sel, values, depth=5)
+            res = {}
+            for loop in (True, False):
+                t.set_device_loop(loop)
+                d, tr = P.adaptive_bfs(g, r, flat, stats)
+                res[loop] = ([(int(x.kernel), int(x.variant), x.fallback_used, x.frontier_size)
+                              for x in tr.records], d.copy())
+            assert res[True][0] == res[False][0]
+            np.testing.assert_array_equal(res[True][1], res[False][1])
+    finally:
+        t.set_device_loop(True)
