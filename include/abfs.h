@@ -183,8 +183,9 @@ ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
 
 /* 1 (default): bfs_full / adaptive_bfs run the whole level loop inside one
  * persistent cooperative kernel (device-side FlatTree, grid barriers between
- * levels; 2 = same with a 48-register / 5-CTA-per-SM budget instead of
- * 40 / 6); 0: one launch chain + one host round trip per level. */
+ * levels; 5 CTAs x 256 threads per SM, 48 registers); 2 = the same with
+ * 6 CTAs / 40 registers, 3 = 4 CTAs / 64 registers; 0: one launch chain +
+ * one host round trip per level. */
 ABFS_API int abfs_traversal_set_mode(abfs_traversal *t, int device_loop);
 
 /* Number of kernels this traversal has launched (bench gpu_launches). */

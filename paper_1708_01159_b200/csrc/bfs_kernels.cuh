@@ -666,29 +666,41 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 }
             }
             __syncwarp();
-            for (uint32_t base = 0; base < total; base += 32) {
-                const bool has = base + lane < total;
-                const uint32_t v = has ? wbuf[base + lane] : 0u;
-                uint32_t j = 0, e = 0, f0 = 0;
-                if (has) {
-                    // the offsets and the first in-neighbour (dense array,
-                    // coalesced over consecutive candidates) load together
-                    j = __ldg(in_off + v);
-                    e = __ldg(in_off + v + 1);
-                    f0 = __ldg(first_src + v);
+            for (uint32_t base = 0; base < total; base += 64) {
+                // probe 0 for two candidates per lane at once: the offsets and
+                // the first in-neighbour (dense array, coalesced over
+                // consecutive candidates) of both, then both frontier bits --
+                // the smallest in-neighbour is a hub on skewed graphs, so
+                // most candidates stop here without touching src
+                uint32_t vv[2], jj[2], ee[2], ff0[2];
+                bool fnd[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const bool has = base + h * 32 + lane < total;
+                    vv[h] = has ? wbuf[base + h * 32 + lane] : 0u;
+                    jj[h] = has ? __ldg(in_off + vv[h]) : 0u;
+                    ee[h] = has ? __ldg(in_off + vv[h] + 1) : 0u;
+                    ff0[h] = has ? __ldg(first_src + vv[h]) : 0u;
                 }
-                // probe 0: the smallest in-neighbour (a hub on skewed graphs,
-                // so most candidates stop here without touching src)
-                bool found = false;
-                if (j < e) {
-                    ++scanned;
-                    if (in_bitmap(c.fbm, f0)) {
-                        found = true;
-                        j = e;
-                    } else {
-                        ++j;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    fnd[h] = false;
+                    if (jj[h] < ee[h]) {
+                        ++scanned;
+                        if (in_bitmap(c.fbm, ff0[h])) {
+                            fnd[h] = true;
+                            jj[h] = ee[h];
+                        } else {
+                            ++jj[h];
+                        }
                     }
                 }
+              for (int h = 0; h < 2; ++h) {
+                if (base + h * 32 >= total) break;   // warp-uniform
+                const uint32_t v = vv[h];
+                uint32_t j = jj[h];
+                const uint32_t e = ee[h];
+                bool found = fnd[h];
                 // phase A: each candidate scans up to pull_light more of its
                 // in-neighbours, one aligned 16-byte load per step (one L1
                 // wavefront per lane instead of four), early exit
@@ -764,6 +776,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                     atomicOr(wfound + ((v >> 5) - wbase), 1u << (v & 31));
                 }
                 em.add(__ballot_sync(kFull, found));
+              }
             }
             __syncwarp();
             if (mine && cand) {

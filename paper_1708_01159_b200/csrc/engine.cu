@@ -76,7 +76,7 @@ struct abfs_traversal {
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
     int mega_grid = 0;
-    int mega_minb = 6;
+    int mega_minb = 5;          // resident CTAs per SM the megakernel is compiled for
     char *stage = nullptr;                     // pinned D2H staging (2 chunks)
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
@@ -673,7 +673,7 @@ static uint64_t rec_ns(const MegaRecord &r) {
 extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
     t->use_mega = device_loop != 0;
-    const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 5 : 6;
+    const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 6 : 5;
     if (minb != t->mega_minb) {
         t->mega_minb = minb;
         t->mega_grid = 0;
