@@ -604,8 +604,11 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
     // 8-word grain at the end of the level (dense levels balance).
     CEmit<VAR> em(sn, c.count);
     const unsigned lane = lane_id();
-    const uint64_t nsub = (words - word0 + kPullSub - 1) / kPullSub;
-    const uint64_t nchunks = (nsub + kPullChunkSubs - 1) / kPullChunkSubs;
+    // word indices fit 32 bits (|V| < 2^32): 32-bit bookkeeping keeps the
+    // megakernel's register pressure down
+    const uint32_t w0 = (uint32_t)word0, wend = (uint32_t)words;
+    const uint32_t nsub = (wend - w0 + kPullSub - 1) / kPullSub;
+    const uint32_t nchunks = (nsub + kPullChunkSubs - 1) / kPullChunkSubs;
     if (threadIdx.x == 0) *sfetch = ((unsigned long long)kFetchInit << 32) | kPullChunkSubs;
     __syncthreads();
     unsigned long long scanned = 0;
@@ -634,12 +637,12 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             cid = (uint32_t)g;
             sidx = 0;
         }
-        const uint64_t sg = (uint64_t)cid * kPullChunkSubs + sidx;
+        const uint32_t sg = cid * kPullChunkSubs + sidx;
         if (sg >= nsub) continue;
         {
-            const uint64_t wbase = word0 + sg * kPullSub;
-            const uint64_t myw = wbase + lane;
-            const bool mine = lane < (unsigned)kPullSub && myw < words;
+            const uint32_t wbase = w0 + sg * kPullSub;
+            const uint32_t myw = wbase + lane;
+            const bool mine = lane < (unsigned)kPullSub && myw < wend;
             uint32_t vis = 0xffffffffu, cand = 0;
             if (mine) {
                 vis = c.visited[myw];
@@ -662,7 +665,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 while (bits) {
                     const int b = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    wbuf[pos++] = (uint32_t)(myw * 32 + b);
+                    wbuf[pos++] = myw * 32 + (uint32_t)b;
                 }
             }
             __syncwarp();
