@@ -322,7 +322,7 @@ def run_ours(a):
 
     # ---- e2e through the public API with host results ----------------------
     e2e = None
-    if rank == 0 or world > 1:
+    if True:
         dg_api = dg
         dg_api._scratch = Traversal(dg)
         n_e2e = min(len(my_roots), R * max(1, a.steps // 2))
@@ -341,6 +341,12 @@ def run_ours(a):
             e_edges += m_trav[r]
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
+        if world > 1:   # whole-job: edges summed over ranks / slowest rank's time
+            te = torch.tensor([e_edges, el], dtype=torch.float64, device="cuda")
+            tmax = te.clone()
+            dist.all_reduce(te)
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            e_edges, el = float(te[0].item()), float(tmax[1].item())
         e2e = {"value": round(e_edges / el / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": int(R * 8 + flat.node_count * 19 + 24 * 8),
                "d2h_bytes_per_step": int(R * 4 * V),
