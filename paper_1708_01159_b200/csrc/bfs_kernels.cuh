@@ -388,13 +388,191 @@ __device__ __forceinline__ void edge_body(const LevelCtx &c, SmemQ *sq,
     em.finish();
 }
 
+// ---------------------------------------------------------------------------
+// TMA-streamed edge list.  The head stream (origins / reverse owners, 4 bytes
+// per slot, read exactly once per level) is moved by the copy engine: one
+// thread arms an mbarrier and issues a 1-D bulk copy (cp.async.bulk) of the
+// CTA's next chunk into a shared-memory stage while the CTA processes the
+// previous one, so the stream's DRAM latency leaves the threads' critical
+// path and registers hold no in-flight stream data.  The per-slot logic is
+// edge_body's (frontier test on sorted origins, dst/src gathered only for
+// active slots, claim + count epilogue).
+// ---------------------------------------------------------------------------
+constexpr int kStreamStages = 2;
+
+// Two-stage ring of CH-slot chunks.  full[s]: armed by the producer with the
+// chunk's byte count, completed by the copy engine.  empty[s]: one arrival
+// per warp once it holds its slots in registers; the producer (thread 0)
+// waits on it before re-filling the stage, so no warp ever waits for another
+// warp's claim work (no CTA-wide barrier per chunk).  Barriers are set up once
+// per kernel; the parity of every stage's next phase is carried in `uses`.
+template <uint32_t CH>
+struct SmemStreamT {
+    uint32_t buf[kStreamStages][CH];
+    unsigned long long full[kStreamStages], empty[kStreamStages];
+    uint32_t uses[kStreamStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait(const unsigned long long *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+
+template <uint32_t CH>
+__device__ __forceinline__ void stream_init(SmemStreamT<CH> *ss) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStreamStages; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&ss->full[s])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                         :: "r"(smem_u32(&ss->empty[s])), "r"(kWarps) : "memory");
+            ss->uses[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+template <uint32_t CH>
+__device__ __forceinline__ void stream_issue(SmemStreamT<CH> *ss, int stage, const uint32_t *src,
+                                             uint32_t bytes) {
+    // generic-proxy reads of this stage (ordered by the empty barrier) before
+    // the async-proxy write
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_u32(&ss->full[stage])), "r"(bytes) : "memory");
+    // evict-first: the 2-4 GB stream must not push the L2-resident bitmaps
+    // (visited / frontier, probed by every claim) out of L2
+    unsigned long long policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(ss->buf[stage])), "l"(src), "r"(bytes),
+                    "r"(smem_u32(&ss->full[stage])), "l"(policy) : "memory");
+}
+
+template <int VAR, bool REV, uint32_t CH>
+__device__ __forceinline__ void edge_stream_body(const LevelCtx &c, SmemQ *sq, SmemStreamT<CH> *ss,
+                                                 const uint32_t *__restrict__ stream_arr,
+                                                 const uint32_t *__restrict__ gather_arr,
+                                                 uint64_t m) {
+    static_assert(CH % (kBlock * 4) == 0, "chunk = whole uint4 groups");
+    QEmit<VAR> em(sq, c.q_next, c.q_tail);
+    const bool consistent = (*c.inconsistent == 0);
+    const uint64_t nchunks = (m + CH - 1) / CH;
+    auto chunk_bytes = [&](uint64_t ch) -> uint32_t {
+        const uint64_t slots = min((uint64_t)CH, m - ch * CH);
+        return (uint32_t)((slots * 4 + 15) & ~15ull);   // arrays are padded by 16 bytes
+    };
+    uint32_t u[kStreamStages];
+#pragma unroll
+    for (int s = 0; s < kStreamStages; ++s) u[s] = ss->uses[s];
+    __syncthreads();   // every thread has read `uses` before thread 0 advances it
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kStreamStages; ++s) {
+            const uint64_t ch = blockIdx.x + (uint64_t)s * gridDim.x;
+            if (ch < nchunks) stream_issue(ss, s, stream_arr + ch * CH, chunk_bytes(ch));
+        }
+    uint32_t k = 0;
+    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++k) {
+        const int stage = (int)(k % kStreamStages);
+        const uint32_t par = (u[stage] + k / kStreamStages) & 1u;
+        mbar_wait(&ss->full[stage], par);
+        const uint64_t tile = ch * CH;
+        constexpr int kGroups = CH / (kBlock * 4);
+        uint4 t4[kGroups];
+#pragma unroll
+        for (int h = 0; h < kGroups; ++h)
+            t4[h] = reinterpret_cast<const uint4 *>(ss->buf[stage])[h * kBlock + threadIdx.x];
+        __syncwarp();
+        if (lane_id() == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
+                         :: "r"(smem_u32(&ss->empty[stage])) : "memory");
+        if (threadIdx.x == 0) {
+            const uint64_t nxt = ch + (uint64_t)kStreamStages * gridDim.x;
+            if (nxt < nchunks) {
+                mbar_wait(&ss->empty[stage], par);   // all warps hold this chunk
+                stream_issue(ss, stage, stream_arr + nxt * CH, chunk_bytes(nxt));
+            }
+        }
+        bool act[kGroups][4];
+        bool any = false;
+#pragma unroll
+        for (int h = 0; h < kGroups; ++h) {
+            const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+            const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
+            if (!REV) {
+                const uint32_t w0 = s4[0] >> 5, w3 = s4[3] >> 5;
+                if (w0 == w3 && e + 3 < m) {
+                    const uint32_t fw = __ldg(c.fbm + w0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) act[h][q] = (fw >> (s4[q] & 31)) & 1u;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) act[h][q] = (e + q < m) && in_bitmap(c.fbm, s4[q]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    act[h][q] = (e + q < m) && claim_possible(c, s4[q], consistent);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) any |= act[h][q];
+        }
+        if (__any_sync(kFull, any)) {  // idle warps skip the claim/emit stage
+#pragma unroll
+            for (int h = 0; h < kGroups; ++h) {
+                const uint64_t e = tile + (uint64_t)h * (kBlock * 4) + threadIdx.x * 4u;
+                const uint32_t s4[4] = {t4[h].x, t4[h].y, t4[h].z, t4[h].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    bool won = false;
+                    uint32_t v = 0;
+                    if (act[h][q]) {
+                        if (!REV) {
+                            v = __ldg(gather_arr + e + q);
+                            won = claim(c, v, consistent);
+                        } else {
+                            v = s4[q];
+                            if (in_bitmap(c.fbm, __ldg(gather_arr + e + q))) won = claim(c, v, consistent);
+                        }
+                    }
+                    em.emit(won, v);
+                }
+            }
+        }
+        em.tile_end();
+    }
+    __syncthreads();   // every wait of this call is done before `uses` advances
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kStreamStages; ++s)
+            ss->uses[s] = u[s] + (k + kStreamStages - 1 - s) / kStreamStages;   // chunks on stage s
+    __syncthreads();
+    em.finish();
+}
+
+// 4 KB stages: the unified L1 / shared memory must keep most of its capacity
+// as L1 (frontier and visited probes of every claim hit there)
+constexpr uint32_t kStreamChunk = 1024;
+using SmemStream = SmemStreamT<kStreamChunk>;
+
 template <int VAR, bool REV>
 __global__ void __launch_bounds__(kBlock)
 k_edge(LevelCtx c, const uint32_t *__restrict__ stream_arr,
        const uint32_t *__restrict__ gather_arr, uint64_t m) {
     __shared__ SmemQ sq;
+    __shared__ __align__(16) SmemStream ss;
     zero_slot(c);
-    edge_body<VAR, REV>(c, &sq, stream_arr, gather_arr, m);
+    stream_init(&ss);
+    edge_stream_body<VAR, REV, kStreamChunk>(c, &sq, &ss, stream_arr, gather_arr, m);
     publish(c);
 }
 
