@@ -588,10 +588,11 @@ template <int VAR>
 __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
                                           const uint32_t *__restrict__ q, uint32_t F,
                                           const uint32_t *__restrict__ out_off,
-                                          const uint32_t *__restrict__ dst) {
+                                          const uint32_t *__restrict__ dst, uint32_t bid,
+                                          uint32_t nblk) {
     QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
-    for (uint32_t base = blockIdx.x * kBlock; base < F; base += gridDim.x * kBlock) {
+    for (uint32_t base = bid * kBlock; base < F; base += nblk * kBlock) {
         const uint32_t i = base + threadIdx.x;
         uint32_t j = 0, e = 0;
         if (i < F) {
@@ -630,7 +631,7 @@ k_push(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
        const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
     zero_slot(c);
-    push_body<VAR>(c, &sq, q, F, out_off, dst);
+    push_body<VAR>(c, &sq, q, F, out_off, dst, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -644,7 +645,8 @@ template <int VAR>
 __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
                                                const uint32_t *__restrict__ q, uint32_t F,
                                                const uint32_t *__restrict__ out_off,
-                                               const uint32_t *__restrict__ dst, int vw_log2) {
+                                               const uint32_t *__restrict__ dst, int vw_log2,
+                                               uint32_t bid, uint32_t nblk) {
     QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     const uint32_t VW = 1u << vw_log2;
@@ -653,7 +655,7 @@ __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
     const unsigned lane = lane_id();
     const uint32_t sub = lane >> vw_log2, sl = lane & (VW - 1);
     const uint32_t wib = threadIdx.x >> 5;
-    for (uint32_t bb = blockIdx.x * per_block; bb < F; bb += gridDim.x * per_block) {
+    for (uint32_t bb = bid * per_block; bb < F; bb += nblk * per_block) {
         const uint32_t i = bb + wib * per + sub;
         uint32_t j = 0, e = 0;
         if (i < F) {
@@ -695,22 +697,23 @@ k_push_warp(LevelCtx c, const uint32_t *__restrict__ q, uint32_t F,
             const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
     zero_slot(c);
-    push_warp_body<VAR>(c, &sq, q, F, out_off, dst, VWL);
+    push_warp_body<VAR>(c, &sq, q, F, out_off, dst, VWL, blockIdx.x, gridDim.x);
 }
 
 template <int VAR>
 __device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
                                            const uint32_t *__restrict__ out_off,
-                                           const uint32_t *__restrict__ dst) {
+                                           const uint32_t *__restrict__ dst, uint32_t bid,
+                                           uint32_t nblk) {
     QEmit<VAR> em(sq, c.q_next, c.q_tail);
     const bool consistent = (*c.inconsistent == 0);
     const unsigned nunits = *(volatile unsigned *)c.units_tail;
     // push units carry their adjacency slice [x, y) directly (no offset
     // lookup); the next unit's descriptor is loaded while this one runs
-    uint2 nxt = blockIdx.x < nunits ? c.units[blockIdx.x] : make_uint2(0, 0);
-    for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
+    uint2 nxt = bid < nunits ? c.units[bid] : make_uint2(0, 0);
+    for (unsigned w = bid; w < nunits; w += nblk) {
         const uint2 un = nxt;
-        if (w + gridDim.x < nunits) nxt = c.units[w + gridDim.x];
+        if (w + nblk < nunits) nxt = c.units[w + nblk];
         const uint32_t b = un.x, e = un.y;
         for (uint32_t jb = b; jb < e; jb += kBlock * 4) {
             uint32_t v[4];
@@ -734,7 +737,7 @@ template <int VAR>
 __global__ void __launch_bounds__(kBlock)
 k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__restrict__ dst) {
     __shared__ SmemQ sq;
-    heavy_body<VAR>(c, &sq, out_off, dst);
+    heavy_body<VAR>(c, &sq, out_off, dst, blockIdx.x, gridDim.x);
     publish(c);
 }
 
@@ -1139,6 +1142,18 @@ static __global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, u
         if (v >= n || in_off[v + 1] == in_off[v]) bits |= 1u << k;
     }
     noin[word] = bits;
+}
+
+// Largest out-degree (decides the megakernel's solo mode).
+static __global__ void k_max_degree(const uint32_t *__restrict__ out_off, uint64_t n,
+                                    unsigned int *out) {
+    unsigned int mx = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        mx = max(mx, out_off[v + 1] - out_off[v]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_down_sync(kFull, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 
 // Rebuild frontier bitmap + visited bitmap from an arbitrary depth array.

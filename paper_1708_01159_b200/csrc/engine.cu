@@ -8,6 +8,7 @@
 // features and the FlatTree (adaptive.py:101-129).
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
@@ -75,7 +76,10 @@ struct abfs_traversal {
     size_t batch_recs = 0;                                   // records kept in mrecs, last launch
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
+    uint64_t max_out_degree = 0;   // decides the megakernel's cluster solo mode
     int mega_grid = 0;
+    int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
+    SoloState *dsolo = nullptr; // solo-mode hand-off (device)
     int mega_minb = 5;          // resident CTAs per SM the megakernel is compiled for
     char *stage = nullptr;                     // pinned D2H staging (2 chunks)
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -297,6 +301,18 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     if (e == cudaSuccess && t->words) {
         k_noin<<<grid_for(t->words, kBlock, 1ull << 31), kBlock>>>(g->d.in_off, n, t->words, t->noin);
         e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) {
+            unsigned int *dmax = nullptr;
+            e = cudaMalloc(&dmax, sizeof(unsigned int));
+            if (e == cudaSuccess) e = cudaMemset(dmax, 0, sizeof(unsigned int));
+            if (e == cudaSuccess) {
+                k_max_degree<<<grid_for(n, kBlock, 148 * 16), kBlock>>>(g->d.out_off, n, dmax);
+                unsigned int h = 0;
+                e = cudaMemcpy(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost);
+                t->max_out_degree = h;
+            }
+            cudaFree(dmax);
+        }
     }
     if (e != cudaSuccess) {
         set_error(std::string("traversal_create: ") + cudaGetErrorString(e));
@@ -321,6 +337,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->units);
     cudaFree(t->dctr);
     cudaFree(t->des);
+    cudaFree(t->dsolo);
     if (t->mrecs) cudaFreeHost(t->mrecs);
     if (t->mnlev) cudaFreeHost(t->mnlev);
     if (t->hroots) cudaFreeHost(t->hroots);
@@ -533,7 +550,37 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
         if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
         t->mega_grid = per * sms;
+        t->mega_cluster = 0;
+        // cluster launch for solo mode: the grid must be whole clusters that
+        // are all co-resident (cooperative)
+        // only on graphs without hubs (max out-degree <= kPushHub): there no
+        // small level ever needs CTA units, so solo levels never hand back;
+        // on skewed graphs the cluster-constrained grid and hub hand-backs
+        // cost more than the solo levels save (measured on Kronecker-24)
+        const char *env = getenv("ABFS_SOLO");
+        const bool want = env ? atoi(env) != 0 : t->max_out_degree <= kPushHub;
+        if (want) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kSoloCluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3((unsigned)(t->mega_grid / kSoloCluster * kSoloCluster));
+            cfg.blockDim = dim3(kBlock);
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters > 0) {
+                t->mega_grid = std::min(t->mega_grid / kSoloCluster, nclusters) * kSoloCluster;
+                t->mega_cluster = kSoloCluster;
+            }
+            if (getenv("ABFS_DEBUG_GRID"))
+                fprintf(stderr, "megakernel grid %d (per SM %d, clusters %d)\n", t->mega_grid, per, nclusters);
+            cudaGetLastError();
+        }
     }
+    if (!t->dsolo) ABFS_CUDA(cudaMalloc(&t->dsolo, sizeof(SoloState)));
     // stage the device tree: static-feature nodes resolved, float64 tests on
     // the per-level features turned into exact integer cutoffs (CutNode)
     PrunedTree pt;
@@ -626,10 +673,29 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.roots = t->droots;
     P.nroots = (uint32_t)nroots;
     P.init_in_kernel = host_init ? 0 : 1;
+    P.solo_ctas = t->mega_cluster ? (uint32_t)t->mega_cluster : 0u;
+    P.solo = t->dsolo;
     for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
-    ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
+    if (t->mega_cluster) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = (unsigned)t->mega_cluster;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)t->mega_grid);
+        cfg.blockDim = dim3(kBlock);
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        ABFS_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
+    } else {
+        ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
+    }
     t->launches += 1;
     ABFS_CUDA(cudaEventRecord(t->ev[1], s));
     ABFS_CUDA(cudaStreamSynchronize(s));

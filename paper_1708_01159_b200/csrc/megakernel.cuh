@@ -54,7 +54,23 @@ struct MegaParams {
     const uint32_t *roots;
     uint32_t nroots;
     int init_in_kernel;
+    // cluster solo mode (0 = off): with a cluster launch, runs of small
+    // top-down levels execute on cluster 0 alone (solo_ctas CTAs, cluster
+    // barriers) while the other CTAs wait at one grid barrier
+    uint32_t solo_ctas;
+    struct SoloState *solo;
 };
+
+// Hand-off from cluster 0 back to the grid after a solo run.
+struct SoloState {
+    unsigned long long frontier, discovered;
+    uint32_t level;
+    int32_t pk, pv, cur, has_q, has_bm, done;
+    uint32_t pad;
+};
+
+constexpr uint32_t kSoloUnits = 16;   // more CTA units than this: hand the level to the grid
+constexpr int kSoloCluster = 8;       // CTAs of cluster 0 (portable cluster size)
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -114,10 +130,10 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         edge_body<VAR, true, 1>(c, sq, P.rev_owner, P.src, P.m);
         break;
     case 2:
-        push_body<VAR>(c, sq, q, F, P.out_off, P.dst);
+        push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, gridDim.x);
         grid.sync();
         if (!units()) return;
-        heavy_body<VAR>(c, sq, P.out_off, P.dst);
+        heavy_body<VAR>(c, sq, P.out_off, P.dst, blockIdx.x, gridDim.x);
         break;
     case 3:
         {
@@ -132,13 +148,30 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
         break;
     default:
-        push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2);
+        push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2, blockIdx.x, gridDim.x);
         grid.sync();
         if (!units()) return;
-        heavy_body<VAR>(c, sq, P.out_off, P.dst);
+        heavy_body<VAR>(c, sq, P.out_off, P.dst, blockIdx.x, gridDim.x);
         break;
     }
     grid.sync();
+}
+
+// One top-down level's light pass on cluster 0 (solo mode).
+template <int VAR>
+__device__ __forceinline__ void solo_light(const MegaParams &P, const LevelCtx &c, int kernel,
+                                           uint32_t F, const uint32_t *q, SmemQ *sq) {
+    if (kernel == 2) push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, P.solo_ctas);
+    else push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2, blockIdx.x, P.solo_ctas);
+}
+
+__device__ __forceinline__ bool solo_fits(const MegaParams &P, int kernel,
+                                          unsigned long long frontier) {
+    // one pass of the cluster's threads (two for virtual warps)
+    const unsigned long long lanes = (unsigned long long)P.solo_ctas * kBlock;
+    if (kernel == 2) return frontier <= lanes;
+    if (kernel == 4) return (frontier << P.vw_log2) <= 2 * lanes;
+    return false;
 }
 
 // MINB = resident CTAs per SM the register budget is sized for (6 -> 40
@@ -203,6 +236,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
     int cur = 0;
     bool has_q = true, has_bm = true;
+    uint32_t solo_skip = 0xffffffffu;
     for (uint32_t level = 0;; ++level) {
         const unsigned long long t0 = lead ? globaltimer() : 0ull;
         if (threadIdx.x == 0)
@@ -223,6 +257,156 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             P.ctr->cq3[zero] = 0;
             P.ctr->es3[zero] = 0;
             P.ctr->work[zero] = 0;
+        }
+        if (P.solo_ctas && has_q && level != solo_skip && solo_fits(P, pk, frontier)) {
+            // ---- cluster solo mode: cluster 0 runs this level and the
+            // following small top-down levels alone (cluster barriers,
+            // ~0.3 us) while every other CTA waits at ONE grid barrier
+            if (blockIdx.x < P.solo_ctas) {
+                cg::cluster_group cl = cg::this_cluster();
+                uint32_t L = level;
+                int fb = fallback;
+                unsigned long long ts = t0, tq = tp;
+                int ppk = pk, ppv = pv;   // pair of the last executed level
+                for (;;) {
+                    const int o = (int)(L % 3), z = (int)((L + 1) % 3);
+                    if (lead && L != level) {
+                        P.ctr->qlen[z] = 0;
+                        P.ctr->units[z] = 0;
+                        P.ctr->count[z] = 0;
+                        P.ctr->cq3[z] = 0;
+                        P.ctr->es3[z] = 0;
+                        P.ctr->work[z] = 0;
+                    }
+                    LevelCtx sc;
+                    sc.depth = P.depth;
+                    sc.visited = P.visited;
+                    sc.fbm = cur ? P.fbm1 : P.fbm0;
+                    sc.q_next = cur ? P.q0 : P.q1;
+                    sc.q_tail = &P.ctr->qlen[o];
+                    sc.count = &P.ctr->count[o];
+                    sc.units_tail = &P.ctr->units[o];
+                    sc.units = P.units;
+                    sc.inconsistent = &P.ctr->inconsistent;
+                    sc.ctr = P.ctr;
+                    sc.mb = nullptr;
+                    sc.es = nullptr;
+                    sc.work = &P.ctr->work[o];
+                    sc.pull_light = P.pull_light;
+                    sc.seq = 0;
+                    sc.zero_slot = z;
+                    sc.level = (int32_t)L;
+                    sc.lvl1 = (int32_t)L + 1;
+                    const uint32_t *qc = cur ? P.q1 : P.q0;
+                    switch (pv) {
+                    case 0: solo_light<0>(P, sc, pk, (uint32_t)frontier, qc, &sq); break;
+                    case 1: solo_light<1>(P, sc, pk, (uint32_t)frontier, qc, &sq); break;
+                    default: solo_light<2>(P, sc, pk, (uint32_t)frontier, qc, &sq); break;
+                    }
+                    cl.sync();
+                    const unsigned nu = *(volatile unsigned *)sc.units_tail;
+                    if (nu > kSoloUnits) {
+                        // hubs in the frontier: the grid redoes this level (its
+                        // claims so far stay counted in qlen[o]; units are rebuilt)
+                        if (lead) {
+                            P.ctr->units[o] = 0;
+                            P.solo->level = L;
+                            P.solo->frontier = frontier;
+                            P.solo->discovered = discovered;
+                            P.solo->pk = ppk;
+                            P.solo->pv = ppv;
+                            P.solo->cur = cur;
+                            P.solo->has_q = 1;
+                            P.solo->has_bm = has_bm ? 1 : 0;
+                            P.solo->done = 0;
+                        }
+                        break;
+                    }
+                    if (nu) {
+                        switch (pv) {
+                        case 0: heavy_body<0>(sc, &sq, P.out_off, P.dst, blockIdx.x, P.solo_ctas); break;
+                        case 1: heavy_body<1>(sc, &sq, P.out_off, P.dst, blockIdx.x, P.solo_ctas); break;
+                        default: heavy_body<2>(sc, &sq, P.out_off, P.dst, blockIdx.x, P.solo_ctas); break;
+                        }
+                        cl.sync();
+                    }
+                    const unsigned long long nw2 = *(volatile unsigned *)sc.q_tail;
+                    if (lead && rec_off + L < P.cap) {
+                        MegaRecord &r = P.recs[rec_off + L];
+                        r.kernel = pk;
+                        r.variant = pv;
+                        r.fallback = fb;
+                        r.converted = 0;
+                        r.frontier = frontier;
+                        r.new_count = nw2;
+                        r.t_start = ts;
+                        r.t_pred = tq;
+                        r.t_end = globaltimer();
+                        r.scanned = 0;
+                    }
+                    ppk = pk;
+                    ppv = pv;
+                    if (nw2 == 0) {
+                        if (lead) {
+                            P.solo->level = L;
+                            P.solo->done = 1;
+                        }
+                        break;
+                    }
+                    frontier = nw2;
+                    discovered += nw2;
+                    cur ^= 1;
+                    has_bm = false;
+                    ++L;
+                    // next level's decision (every cluster CTA, same result)
+                    ts = lead ? globaltimer() : 0ull;
+                    if (threadIdx.x == 0)
+                        s_cls = P.fixed_pair >= 0 ? P.fixed_pair
+                                                  : mega_tree_class(T, frontier, discovered);
+                    __syncthreads();
+                    const int ncls = s_cls;
+                    fb = ncls == 254;
+                    const int npk = fb ? pk : ncls / 3, npv = fb ? pv : ncls % 3;
+                    if (!solo_fits(P, npk, frontier)) {
+                        if (lead) {
+                            P.solo->level = L;
+                            P.solo->frontier = frontier;
+                            P.solo->discovered = discovered;
+                            P.solo->pk = ppk;
+                            P.solo->pv = ppv;
+                            P.solo->cur = cur;
+                            P.solo->has_q = 1;
+                            P.solo->has_bm = 0;
+                            P.solo->done = 0;
+                        }
+                        break;
+                    }
+                    pk = npk;
+                    pv = npv;
+                    tq = lead ? globaltimer() : 0ull;
+                }
+            }
+            grid.sync();
+            {
+                volatile SoloState *st = P.solo;
+                const uint32_t L = st->level;
+                if (st->done) {
+                    if (lead) P.n_levels[ri] = (unsigned long long)L + 1;
+                    rec_off += L + 1;
+                    break;
+                }
+                frontier = st->frontier;
+                discovered = st->discovered;
+                pk = st->pk;
+                pv = st->pv;
+                cur = st->cur;
+                has_q = st->has_q != 0;
+                has_bm = st->has_bm != 0;
+                solo_skip = L;   // the grid runs level L (never solo again)
+                level = L - 1;   // ++level
+            }
+            grid.sync();         // everyone has read the hand-off before it is reused
+            continue;
         }
         uint32_t *fbm_cur = cur ? P.fbm1 : P.fbm0, *fbm_nxt = cur ? P.fbm0 : P.fbm1;
         uint32_t *q_cur = cur ? P.q1 : P.q0, *q_nxt = cur ? P.q0 : P.q1;
