@@ -185,7 +185,9 @@ ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
  * persistent cooperative kernel (device-side FlatTree, grid barriers between
  * levels; 5 CTAs x 256 threads per SM, 48 registers); 2 = the same with
  * 6 CTAs / 40 registers, 3 = 4 CTAs / 64 registers; 0: one launch chain +
- * one host round trip per level. */
+ * one host round trip per level.  On graphs with max out-degree <= 64 the
+ * megakernel also runs small levels on one 8-CTA cluster ("solo mode";
+ * environment ABFS_SOLO=0/1 forces it off/on). */
 ABFS_API int abfs_traversal_set_mode(abfs_traversal *t, int device_loop);
 
 /* Number of kernels this traversal has launched (bench gpu_launches). */

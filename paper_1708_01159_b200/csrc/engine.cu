@@ -575,8 +575,6 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
                 t->mega_grid = std::min(t->mega_grid / kSoloCluster, nclusters) * kSoloCluster;
                 t->mega_cluster = kSoloCluster;
             }
-            if (getenv("ABFS_DEBUG_GRID"))
-                fprintf(stderr, "megakernel grid %d (per SM %d, clusters %d)\n", t->mega_grid, per, nclusters);
             cudaGetLastError();
         }
     }
