@@ -42,7 +42,17 @@ __global__ void k(const uint32_t *a, uint64_t m, unsigned long long *sum, unsign
         __syncthreads();
         if (threadIdx.x == 0) { uint64_t nx = ch + (uint64_t)kStages * gridDim.x; if (nx < nch) issue<FP>(&ss, st, a + nx * kChunk, bytes(nx)); }
     }
-    atomicAdd(sum, loc);
+    // block reduce, one atomic per CTA (a per-thread atomic on one address
+    // would dominate the kernel)
+    __shared__ unsigned long long part[32];
+    for (int o = 16; o > 0; o >>= 1) loc += __shfl_down_sync(0xffffffffu, loc, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+        atomicAdd(sum, t);
+    }
 }
 int main() {
     for (uint64_t m : {1000ull, 2048ull, 100000ull, 1ull << 27}) {
