@@ -260,6 +260,22 @@ ABFS_API int abfs_part_level_p2p(abfs_part *p, int64_t level, int kernel, int va
 ABFS_API int abfs_part_p2p_finish(abfs_part *p, uint64_t *global_count, uint64_t *local_count,
                                   uint64_t *elapsed_ns);
 
+/* Whole traversals over fused-exchange partitions of this process (peers
+ * set), driven in C with no Python per level: adaptive_bfs
+ * (adaptive.py:83-129, tree on the reference's float64 features) and
+ * bfs_full (kernels.py:356-371).  records[l] as abfs_adaptive_bfs
+ * (elapsed_ns = slowest partition's level time incl. the exchange);
+ * local_counts (optional, cap x nparts) = each partition's count of each
+ * level through its count variant. */
+ABFS_API int abfs_parts_adaptive_bfs(abfs_part *const *parts, uint32_t nparts, int64_t root,
+                                     const abfs_tree *tree, const double *static24,
+                                     int64_t chunk_size, abfs_level_record *records,
+                                     uint64_t *local_counts, size_t cap, size_t *n_levels);
+ABFS_API int abfs_parts_bfs_full(abfs_part *const *parts, uint32_t nparts, int64_t root,
+                                 int kernel, int variant, int64_t chunk_size,
+                                 abfs_level_record *records, uint64_t *local_counts, size_t cap,
+                                 size_t *n_levels);
+
 /* Owned depths (hi - lo entries) to host / to a device buffer (async). */
 ABFS_API int abfs_part_read_depths(abfs_part *p, int32_t *host_owned);
 ABFS_API int abfs_part_depths_device(abfs_part *p, int32_t *dev_out);

@@ -111,6 +111,14 @@ _SIGNATURES = {
     "abfs_part_level_p2p": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_int64]),
     "abfs_part_p2p_finish": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p, u64p]),
+    "abfs_parts_adaptive_bfs": (ctypes.c_int, [vpp, ctypes.c_uint32, ctypes.c_int64,
+                                               ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
+                                               ctypes.POINTER(AbfsLevelRecord), u64p, ctypes.c_size_t,
+                                               ctypes.POINTER(ctypes.c_size_t)]),
+    "abfs_parts_bfs_full": (ctypes.c_int, [vpp, ctypes.c_uint32, ctypes.c_int64, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int64,
+                                           ctypes.POINTER(AbfsLevelRecord), u64p, ctypes.c_size_t,
+                                           ctypes.POINTER(ctypes.c_size_t)]),
     "abfs_host_register": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
     "abfs_host_unregister": (ctypes.c_int, [ctypes.c_void_p]),
 }

@@ -720,3 +720,88 @@ extern "C" int abfs_part_p2p_finish(abfs_part *p, uint64_t *global_count, uint64
     p->last_kernel = -1;
     return ABFS_OK;
 }
+
+// ---- whole traversals over fused-exchange partitions (no host per level) --
+
+// adaptive_bfs (adaptive.py:83-129) / bfs_full (kernels.py:356-371) driven in
+// C over the partitions this process owns: per level every partition's
+// strategy + peer push is enqueued, then every partition's device wait; the
+// tree is evaluated on the reference's float64 features between levels.
+static int parts_traverse(abfs_part *const *parts, uint32_t nparts, int64_t root,
+                          const abfs_tree *tr, const double *static24, int fixed_pair,
+                          int64_t chunk, abfs_level_record *recs, uint64_t *local_counts,
+                          size_t cap, size_t *n_levels) {
+    if (!parts || !nparts || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    for (uint32_t i = 0; i < nparts; ++i) {
+        if (!parts[i]) return fail(ABFS_EINVAL, "null partition");
+        if (!parts[i]->nranks)
+            return fail(ABFS_EINVAL, "peers not set (abfs_part_set_peers / abfs_part_ipc_open)");
+        ABFS_TRY(abfs_part_init(parts[i], root));
+    }
+    uint64_t frontier = 1, discovered = 1;
+    int pk = ABFS_EDGE_LIST, pv = ABFS_DIRECT_ATOMIC;   // DEFAULT_KERNEL adaptive.py:36-38
+    std::vector<double> canon(ABFS_N_FEATURES), proj(tr ? tr->n_selection : 0);
+    for (int64_t level = 0;; ++level) {
+        int fallback = 0;
+        if (fixed_pair >= 0) {
+            pk = fixed_pair / 3;
+            pv = fixed_pair % 3;
+        } else {
+            ABFS_TRY(abfs_features(static24, frontier, discovered, canon.data()));
+            for (uint32_t k = 0; k < tr->n_selection; ++k) proj[k] = canon[tr->selection[k]];
+            int cls = 0;
+            ABFS_TRY(abfs_tree_predict(tr, proj.data(), &cls));
+            fallback = cls == ABFS_LEAF_UNKNOWN;
+            if (!fallback) {
+                pk = cls / 3;
+                pv = cls % 3;
+            }
+        }
+        for (uint32_t i = 0; i < nparts; ++i) ABFS_TRY(abfs_part_level_p2p(parts[i], level, pk, pv, chunk));
+        uint64_t g = 0, ns = 0;
+        for (uint32_t i = 0; i < nparts; ++i) {
+            uint64_t gi = 0, li = 0, nsi = 0;
+            ABFS_TRY(abfs_part_p2p_finish(parts[i], &gi, &li, &nsi));
+            if (i && gi != g) return fail(ABFS_ENCCL, "partitions disagree on the level count");
+            g = gi;
+            if (local_counts && (size_t)level < cap) local_counts[(size_t)level * nparts + i] = li;
+            ns = nsi > ns ? nsi : ns;
+        }
+        if (recs && (size_t)level < cap) {
+            abfs_level_record &r = recs[level];
+            r.level = level;
+            r.kernel = pk;
+            r.variant = pv;
+            r.fallback = fallback;
+            r.converted = 0;
+            r.frontier_size = frontier;
+            r.new_count = g;
+            r.elapsed_ns = ns;
+            r.prediction_ns = 1;
+        }
+        if (g == 0) {
+            *n_levels = (size_t)level + 1;
+            return ABFS_OK;
+        }
+        frontier = g;
+        discovered += g;
+    }
+}
+
+extern "C" int abfs_parts_adaptive_bfs(abfs_part *const *parts, uint32_t nparts, int64_t root,
+                                       const abfs_tree *tree, const double *static24,
+                                       int64_t chunk_size, abfs_level_record *records,
+                                       uint64_t *local_counts, size_t cap, size_t *n_levels) {
+    if (!tree || !static24) return fail(ABFS_EINVAL, "null argument");
+    return parts_traverse(parts, nparts, root, tree, static24, -1, chunk_size, records,
+                          local_counts, cap, n_levels);
+}
+
+extern "C" int abfs_parts_bfs_full(abfs_part *const *parts, uint32_t nparts, int64_t root,
+                                   int kernel, int variant, int64_t chunk_size,
+                                   abfs_level_record *records, uint64_t *local_counts, size_t cap,
+                                   size_t *n_levels) {
+    ABFS_TRY(level_params_ok(0, kernel, variant, chunk_size));
+    return parts_traverse(parts, nparts, root, nullptr, nullptr, kernel * 3 + variant, chunk_size,
+                          records, local_counts, cap, n_levels);
+}

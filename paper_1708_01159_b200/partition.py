@@ -279,6 +279,9 @@ class PartitionedBFS:
         self.exchange = exchange
         self.fused = bool(getattr(exchange, "fused", False))
         self.sends = [] if self.fused else [alloc(self.stride) for _ in self.parts]
+        # fused exchange over engine partitions: whole traversals run in C
+        # (abfs_parts_*), no Python between levels
+        self.native = self.fused and all(isinstance(p, DevicePartition) for p in self.parts)
         self.stream = stream
         self.last_local_counts: list[list[int]] = []
         # optional: CUDA-event time of the all-gathers (bench NVLink figure)
@@ -324,10 +327,31 @@ class PartitionedBFS:
             p.init(root)
 
     # -- reference-shaped entry points ------------------------------------------
+    def _native_records(self, fn, *args):
+        cap = 1 << 16
+        if getattr(self, "_native_buf", None) is None:
+            self._native_buf = ((L.AbfsLevelRecord * cap)(),
+                                np.zeros(cap * len(self.parts), np.uint64))
+        recs, loc = self._native_buf
+        nl = ctypes.c_size_t()
+        handles = (ctypes.c_void_p * len(self.parts))(*[p._h.value for p in self.parts])
+        L.check(fn(handles, len(self.parts), *args, recs, L.ptr(loc, L.u64p), cap,
+                   ctypes.byref(nl)), fn.__name__)
+        k = min(nl.value, cap)
+        self.last_local_counts = loc[:k * len(self.parts)].reshape(k, len(self.parts)).tolist()
+        return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:k]]
+
     def bfs_full(self, root: int, kernel: KernelId, variant: CountVariant,
                  chunk_size: int = GROUP_SIZE) -> list[LevelOutcome]:
         """bfs_full (kernels.py:356-371) over the partitions; depths stay
         distributed (see `depths`)."""
+        if self.native:
+            if not 0 <= root < self.n:
+                raise ValueError(f"root {root} out of range for |V|={self.n}")
+            recs = self._native_records(L.lib().abfs_parts_bfs_full, int(root), int(kernel),
+                                        int(variant), int(chunk_size))
+            return [LevelOutcome(new_frontier_count=int(r.new_count), elapsed_ns=int(r.elapsed_ns))
+                    for r in recs]
         self._init(root)
         outs = []
         level = 0
@@ -342,6 +366,19 @@ class PartitionedBFS:
                  chunk_size: int = GROUP_SIZE) -> AdaptiveTrace:
         """adaptive_bfs (adaptive.py:83-129): features from the global counts,
         UNKNOWN falls back to the previous pair, seeded with DEFAULT_KERNEL."""
+        if isinstance(model, FlatTree) and self.native:
+            if not 0 <= root < self.n:
+                raise ValueError(f"root {root} out of range for |V|={self.n}")
+            from .features import static_vector
+            st = np.ascontiguousarray(static_vector(stats), dtype=np.float64)
+            recs = self._native_records(L.lib().abfs_parts_adaptive_bfs, int(root),
+                                        ctypes.byref(model.as_abfs()), L.ptr(st, L.f64p),
+                                        int(chunk_size))
+            return AdaptiveTrace(tuple(
+                LevelTrace(level=int(r.level), kernel=KernelId(r.kernel),
+                           variant=CountVariant(r.variant), fallback_used=bool(r.fallback),
+                           frontier_size=int(r.frontier_size), elapsed_ns=int(r.elapsed_ns),
+                           prediction_ns=int(r.prediction_ns)) for r in recs))
         if isinstance(model, FlatTree):
             policy = lambda level, fv: predict(model, fv)  # noqa: E731
         else:
