@@ -276,6 +276,18 @@ ABFS_API int abfs_parts_bfs_full(abfs_part *const *parts, uint32_t nparts, int64
                                  abfs_level_record *records, uint64_t *local_counts, size_t cap,
                                  size_t *n_levels);
 
+/* The same traversals for ONE partition per process (one GPU) inside the
+ * persistent megakernel: levels, tree decisions and the fused exchange (peer
+ * stores, device-side mailbox wait) all on the device, one launch per
+ * traversal.  Every rank calls it with the same root and tree. */
+ABFS_API int abfs_part_mega_adaptive_bfs(abfs_part *p, int64_t root, const abfs_tree *tree,
+                                         const double *static24, int64_t chunk_size,
+                                         abfs_level_record *records, uint64_t *local_counts,
+                                         size_t cap, size_t *n_levels);
+ABFS_API int abfs_part_mega_bfs_full(abfs_part *p, int64_t root, int kernel, int variant,
+                                     int64_t chunk_size, abfs_level_record *records,
+                                     uint64_t *local_counts, size_t cap, size_t *n_levels);
+
 /* Owned depths (hi - lo entries) to host / to a device buffer (async). */
 ABFS_API int abfs_part_read_depths(abfs_part *p, int32_t *host_owned);
 ABFS_API int abfs_part_depths_device(abfs_part *p, int32_t *dev_out);

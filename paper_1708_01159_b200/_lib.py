@@ -115,6 +115,14 @@ _SIGNATURES = {
                                                ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
                                                ctypes.POINTER(AbfsLevelRecord), u64p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]),
+    "abfs_part_mega_adaptive_bfs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64,
+                                                   ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
+                                                   ctypes.POINTER(AbfsLevelRecord), u64p,
+                                                   ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "abfs_part_mega_bfs_full": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int64,
+                                               ctypes.POINTER(AbfsLevelRecord), u64p, ctypes.c_size_t,
+                                               ctypes.POINTER(ctypes.c_size_t)]),
     "abfs_parts_bfs_full": (ctypes.c_int, [vpp, ctypes.c_uint32, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_int64,
                                            ctypes.POINTER(AbfsLevelRecord), u64p, ctypes.c_size_t,

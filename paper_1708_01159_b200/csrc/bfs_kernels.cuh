@@ -32,6 +32,18 @@
 
 namespace abfs {
 
+// Receiving side of the fused frontier exchange of a vertex partition
+// (partition.cu, megakernel.cuh): every rank adds 1 to `arrive` per level
+// (after its bitmap stores are visible system-wide) and writes its level
+// count into counts[parity][rank].
+struct PeerBox {
+    unsigned long long arrive;
+    unsigned long long pad[7];
+    unsigned long long counts[2][64];
+    unsigned long long local;      // this rank's own count (accumulator)
+    unsigned int timeout;          // set if a wait gave up
+};
+
 // Device counters.  Slots rotate per level call so that no separate zeroing
 // launch is needed: call c appends into slot c%3 and zeroes slot (c+1)%3.
 struct Ctr {

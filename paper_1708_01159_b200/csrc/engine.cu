@@ -523,6 +523,57 @@ static uint32_t prune_node(const abfs_tree *tr, const double *st, uint32_t node,
 // roots: nroots >= 1 traversals run back to back in one launch; with
 // host_init the host ran init_depths for the single root, otherwise every
 // root's init runs inside the kernel.  n_levels = the last root's level count.
+namespace abfs {
+// The device tree of the megakernel for a graph with n vertices (CutNode
+// array; one zero node when there is no tree).
+void stage_cut_tree(const abfs_tree *tr, const double *static24, uint64_t n,
+                    std::vector<unsigned char> &blob, uint32_t &nn) {
+    PrunedTree pt;
+    if (tr && static24) prune_node(tr, static24, 0, pt);
+    nn = (uint32_t)pt.cls.size();
+    blob.assign((nn ? nn : 1) * sizeof(CutNode), 0);
+    if (!nn) return;
+    const double nv = (double)(unsigned long long)static24[0];
+    CutNode *cn = reinterpret_cast<CutNode *>(blob.data());
+    for (uint32_t k = 0; k < nn; ++k) {
+        cn[k].cls = pt.cls[k];
+        cn[k].left = pt.left[k];
+        cn[k].right = pt.right[k];
+        if (pt.cls[k] != ABFS_NOT_A_LEAF) continue;
+        const int canon = tr->selection[pt.feat[k]];
+        const double thr = pt.thr[k];
+        const bool pct = canon == 3 || canon == 5;
+        cn[k].on_disc = (canon == 4 || canon == 5) ? 1 : 0;
+        // smallest k in [0, n] failing "x(k) < thr" (n + 1 if none does)
+        auto holds = [&](uint64_t x) { return pct ? ((double)x / nv < thr) : ((double)x < thr); };
+        uint64_t lo = 0, hi = n + 1;
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (holds(mid)) lo = mid + 1;
+            else hi = mid;
+        }
+        cn[k].cutoff = lo;
+    }
+}
+
+// Plain cooperative launch of the default megakernel variant (partitions).
+int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device) {
+    static int grid = 0;
+    void *kfn = (void *)k_mega<5>;
+    if (!grid) {
+        int per = 0, sms = 0;
+        ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
+        ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
+        grid = per * sms;
+    }
+    MegaParams Q = P;
+    void *args[] = {&Q};
+    ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kBlock), args, 0, s));
+    return ABFS_OK;
+}
+}  // namespace abfs
+
 static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, bool host_init,
                     int fixed_pair, const abfs_tree *tr, const double *static24, int64_t chunk,
                     size_t *n_levels) {
@@ -581,10 +632,10 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     if (!t->dsolo) ABFS_CUDA(cudaMalloc(&t->dsolo, sizeof(SoloState)));
     // stage the device tree: static-feature nodes resolved, float64 tests on
     // the per-level features turned into exact integer cutoffs (CutNode)
-    PrunedTree pt;
-    if (tr && static24) prune_node(tr, static24, 0, pt);
-    const uint32_t nn = (uint32_t)pt.cls.size();
-    const size_t bytes = (nn ? nn : 1) * sizeof(CutNode);
+    std::vector<unsigned char> blob;
+    uint32_t nn = 0;
+    stage_cut_tree(tr, static24, g.n, blob, nn);
+    const size_t bytes = blob.size();
     if (bytes > t->tree_cap) {
         cudaFree(t->dtree);
         if (t->htree) cudaFreeHost(t->htree);
@@ -594,33 +645,6 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaMalloc(&t->dtree, bytes * 2));
         ABFS_CUDA(cudaMallocHost(&t->htree, bytes * 2));
         t->tree_cap = bytes * 2;
-    }
-    std::vector<unsigned char> blob(bytes, 0);
-    if (nn) {
-        const uint64_t n = g.n;
-        const double nv = (double)(unsigned long long)static24[0];
-        CutNode *cn = reinterpret_cast<CutNode *>(blob.data());
-        for (uint32_t k = 0; k < nn; ++k) {
-            cn[k].cls = pt.cls[k];
-            cn[k].left = pt.left[k];
-            cn[k].right = pt.right[k];
-            if (pt.cls[k] != ABFS_NOT_A_LEAF) continue;
-            const int canon = tr->selection[pt.feat[k]];
-            const double thr = pt.thr[k];
-            const bool pct = canon == 3 || canon == 5;
-            cn[k].on_disc = (canon == 4 || canon == 5) ? 1 : 0;
-            // smallest k in [0, n] failing "x(k) < thr" (n + 1 if none does)
-            auto holds = [&](uint64_t x) {
-                return pct ? ((double)x / nv < thr) : ((double)x < thr);
-            };
-            uint64_t lo = 0, hi = n + 1;
-            while (lo < hi) {
-                const uint64_t mid = lo + (hi - lo) / 2;
-                if (holds(mid)) lo = mid + 1;
-                else hi = mid;
-            }
-            cn[k].cutoff = lo;
-        }
     }
     if (blob != t->last_blob) {
         // every mega_run ends with a stream sync, so the pinned staging copy
@@ -673,6 +697,22 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.init_in_kernel = host_init ? 0 : 1;
     P.solo_ctas = t->mega_cluster ? (uint32_t)t->mega_cluster : 0u;
     P.solo = t->dsolo;
+    P.part = 0;
+    P.m_rev = g.m;
+    P.lo = 0;
+    P.hi = g.n;
+    P.wlo = 0;
+    P.wend = t->words;
+    P.vprev = nullptr;
+    P.fnext = nullptr;
+    P.peer_fbm = nullptr;
+    P.peer_box = nullptr;
+    P.box = nullptr;
+    P.nranks = 0;
+    P.rank = 0;
+    P.xcount = nullptr;
+    P.gcount = nullptr;
+    P.xseq0 = 0;
     for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};

@@ -15,6 +15,8 @@
 
 #include <cooperative_groups.h>
 
+#include <vector>
+
 #include "bfs_kernels.cuh"
 
 namespace abfs {
@@ -59,6 +61,26 @@ struct MegaParams {
     // barriers) while the other CTAs wait at one grid barrier
     uint32_t solo_ctas;
     struct SoloState *solo;
+    // ---- vertex partition (part = 1; partition.cu): this rank owns
+    // destinations [lo, hi); depth / visited / noin / in_off / first_src are
+    // rebased to global ids, out_off / dst / org are the destination-filtered
+    // forward slice (m slots), in_off / src / rev_owner the owned reverse
+    // rows (m_rev slots); the frontier bitmaps fbm0/1 are global (words).
+    // After every level the visited bits gained are stored into every rank's
+    // next-frontier bitmap (peer memory) and the global count is summed from
+    // the ranks' mailboxes.  Single graph: lo = 0, hi = n, m_rev = m,
+    // wlo = 0, wend = words, part = 0.
+    int part;
+    uint64_t m_rev, lo, hi, wlo, wend;
+    uint32_t *vprev;            // [wend - wlo] visited words at the previous exchange
+    uint32_t *fnext;            // pull's next-frontier words (rebased); single: unused
+    uint32_t *const *peer_fbm;  // [2][nranks]
+    PeerBox *const *peer_box;   // [nranks]
+    PeerBox *box;
+    uint32_t nranks, rank;
+    unsigned long long *xcount; // slice popc accumulator
+    unsigned long long *gcount; // global level count of the last exchange
+    unsigned long long xseq0;   // exchanges completed before this launch
 };
 
 // Hand-off from cluster 0 back to the grid after a solo run.
@@ -69,6 +91,12 @@ struct SoloState {
     uint32_t pad;
 };
 
+// Host helpers (engine.cu).
+void stage_cut_tree(const abfs_tree *tr, const double *static24, uint64_t n,
+                    std::vector<unsigned char> &blob, uint32_t &nn);
+int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device);
+
+constexpr uint32_t kMegaCapPart = 1u << 16;   // level records of a partition's loop
 constexpr uint32_t kSoloUnits = 16;   // more CTA units than this: hand the level to the grid
 constexpr int kSoloCluster = 8;       // CTAs of cluster 0 (portable cluster size)
 
@@ -127,7 +155,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         edge_body<VAR, false, 1>(c, sq, P.org, P.dst, P.m);
         break;
     case 1:
-        edge_body<VAR, true, 1>(c, sq, P.rev_owner, P.src, P.m);
+        edge_body<VAR, true, 1>(c, sq, P.rev_owner, P.src, P.m_rev);
         break;
     case 2:
         push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, gridDim.x);
@@ -140,7 +168,7 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
             // the pull scratch lists alias the (idle) CTA queue buffer
             static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");
             const unsigned w = threadIdx.x >> 5;
-            pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, 0, P.words,
+            pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, P.wlo, P.wend,
                            sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
         }
         grid.sync();
@@ -200,24 +228,31 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     }
     __syncthreads();
     unsigned long long rec_off = 0;
+    unsigned long long xseq = P.xseq0;   // fused exchanges so far (partition mode)
     for (uint32_t ri = 0; ri < P.nroots; ++ri) {
     if (P.init_in_kernel) {
         // init_depths (kernels.py:134-140) + frontier {root}, as k_init
         const uint32_t root = P.roots[ri];
         const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
         const uint64_t nt = (uint64_t)gridDim.x * kBlock;
-        const uint64_t n4 = P.n / 4;
-        const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
-        for (uint64_t i = tid; i < n4; i += nt) reinterpret_cast<int4 *>(P.depth)[i] = inf4;
-        for (uint64_t i = n4 * 4 + tid; i < P.n; i += nt) P.depth[i] = kInf;
-        for (uint64_t w = tid; w < P.words; w += nt) {
-            const uint32_t bits = (w == (root >> 5)) ? 1u << (root & 31) : 0u;
-            P.visited[w] = bits;
-            P.fbm0[w] = bits;
+        const bool owned = root >= P.lo && root < P.hi;
+        if (!P.part) {
+            const uint64_t n4 = P.n / 4;
+            const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+            for (uint64_t i = tid; i < n4; i += nt) reinterpret_cast<int4 *>(P.depth)[i] = inf4;
+            for (uint64_t i = n4 * 4 + tid; i < P.n; i += nt) P.depth[i] = kInf;
+        } else {
+            for (uint64_t i = P.lo + tid; i < P.hi; i += nt) P.depth[i] = kInf;
         }
+        for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
+            const uint32_t bits = (owned && w == (root >> 5)) ? 1u << (root & 31) : 0u;
+            P.visited[w] = bits;
+            if (P.part) P.vprev[w - P.wlo] = bits;
+        }
+        for (uint64_t w = tid; w < P.words; w += nt) P.fbm0[w] = (w == (root >> 5)) ? 1u << (root & 31) : 0u;
         grid.sync();
         if (lead) {
-            P.depth[root] = 0;
+            if (owned) P.depth[root] = 0;
             P.q0[0] = root;
             for (int s = 0; s < 3; ++s) {
                 P.ctr->qlen[s] = 0;
@@ -453,15 +488,66 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.zero_slot = zero;
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
+        uint32_t *pull_next = P.part ? P.fnext : fbm_nxt;
         switch (pv) {
-        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
-        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
-        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, fbm_nxt, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
         }
         const bool topdown = pk != 3;
-        const unsigned long long nw = topdown
-            ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
-            : *(volatile unsigned long long *)&P.ctr->count[out];
+        unsigned long long nw;
+        if (P.part) {
+            // fused frontier exchange: the visited bits this rank gained are
+            // stored into every rank's next-frontier bitmap over peer memory,
+            // then the ranks' counts are summed through the mailboxes
+            const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+            const uint64_t nt = (uint64_t)gridDim.x * kBlock;
+            uint32_t *const *nxt_tab = P.peer_fbm + (size_t)(cur ^ 1) * P.nranks;
+            unsigned long long cnt = 0;
+            for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
+                const uint32_t v = P.visited[w];
+                const uint32_t x = v & ~P.vprev[w - P.wlo];
+                P.vprev[w - P.wlo] = v;
+                for (uint32_t r = 0; r < P.nranks; ++r) nxt_tab[r][w] = x;
+                cnt += __popc(x);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
+            if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(P.xcount, cnt);
+            __threadfence_system();   // this thread's peer stores before the signal
+            grid.sync();
+            if (lead) {
+                __threadfence_system();
+                const unsigned long long tot = *(volatile unsigned long long *)P.xcount;
+                *(volatile unsigned long long *)P.xcount = 0;
+                const int par = (int)(xseq & 1);
+                for (uint32_t r = 0; r < P.nranks; ++r)
+                    *(volatile unsigned long long *)&P.peer_box[r]->counts[par][P.rank] = tot;
+                __threadfence_system();
+                for (uint32_t r = 0; r < P.nranks; ++r) atomicAdd_system(&P.peer_box[r]->arrive, 1ull);
+                const unsigned long long expect = (xseq + 1) * P.nranks, tw = globaltimer();
+                bool ok = true;
+                while (*(volatile unsigned long long *)&P.box->arrive < expect) {
+                    if (globaltimer() - tw > 20000000000ull) {   // a rank never arrived
+                        P.box->timeout = 1;
+                        ok = false;
+                        break;
+                    }
+                    __nanosleep(100);
+                }
+                __threadfence_system();
+                unsigned long long g = 0;
+                for (uint32_t r = 0; r < P.nranks; ++r)
+                    g += *(volatile unsigned long long *)&P.box->counts[par][r];
+                *(volatile unsigned long long *)P.gcount = ok ? g : 0ull;   // 0 ends the traversal
+            }
+            ++xseq;
+            grid.sync();
+            nw = *(volatile unsigned long long *)P.gcount;
+        } else {
+            nw = topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
+                         : *(volatile unsigned long long *)&P.ctr->count[out];
+        }
 #ifdef ABFS_NO_RECORDS   // overhead experiment only
         if (false) {
 #else
@@ -477,7 +563,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.t_start = t0;
             r.t_pred = tp;
             r.t_end = globaltimer();
-            r.scanned = P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;
+            // partitions: this rank's count through the level's count variant
+            r.scanned = P.part ? (topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
+                                          : *(volatile unsigned long long *)&P.ctr->count[out])
+                      : P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;
         }
         if (nw == 0) {
             if (lead) P.n_levels[ri] = (unsigned long long)level + 1;
@@ -487,8 +576,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         frontier = nw;
         discovered += nw;
         cur ^= 1;
-        has_q = topdown;
-        has_bm = !topdown;
+        has_q = P.part ? false : topdown;   // a partition's next frontier is the gathered bitmap
+        has_bm = P.part ? true : !topdown;
     }
     }   // roots
 }

@@ -29,21 +29,10 @@
 #include <vector>
 
 #include "launch.cuh"
+#include "megakernel.cuh"
 
 using namespace abfs;
 
-namespace abfs {
-// Receiving side of the fused exchange: every rank adds 1 to `arrive` per
-// level (after its bitmap stores are visible system-wide) and writes its
-// level count into counts[parity][rank].
-struct PeerBox {
-    unsigned long long arrive;
-    unsigned long long pad[7];
-    unsigned long long counts[2][64];
-    unsigned long long local;      // this rank's own count (push kernel accumulator)
-    unsigned int timeout;          // set if the wait gave up
-};
-}  // namespace abfs
 
 struct abfs_part {
     int device = 0;
@@ -78,6 +67,14 @@ struct abfs_part {
     unsigned int *pack_ticket = nullptr;         // last-CTA ticket of the push kernel
     unsigned long long p2p_seq = 0;              // exchanges done (every rank agrees)
     std::vector<void *> ipc_opened;              // peer allocations mapped by IPC
+    // persistent per-rank level loop (abfs_part_mega_*)
+    uint32_t *q2 = nullptr;                      // second global-size queue
+    MegaRecord *mrecs = nullptr, *drecs = nullptr;
+    unsigned long long *mnlev = nullptr, *dnlev = nullptr;
+    uint32_t *droots = nullptr;
+    unsigned char *dtree = nullptr;
+    size_t tree_cap = 0;
+    unsigned long long *dx = nullptr;            // {xcount, gcount}
 };
 
 namespace {
@@ -286,6 +283,12 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
     for (void *x : dev) cudaFree(x);
     for (void *x : p->ipc_opened) cudaIpcCloseMemHandle(x);
     cudaFree(p->box);
+    cudaFree(p->q2);
+    if (p->mrecs) cudaFreeHost(p->mrecs);
+    if (p->mnlev) cudaFreeHost(p->mnlev);
+    cudaFree(p->droots);
+    cudaFree(p->dtree);
+    cudaFree(p->dx);
     cudaFree(p->peer_fbm);
     cudaFree(p->peer_box);
     cudaFree(p->pack_ticket);
@@ -804,4 +807,146 @@ extern "C" int abfs_parts_bfs_full(abfs_part *const *parts, uint32_t nparts, int
     ABFS_TRY(level_params_ok(0, kernel, variant, chunk_size));
     return parts_traverse(parts, nparts, root, nullptr, nullptr, kernel * 3 + variant, chunk_size,
                           records, local_counts, cap, n_levels);
+}
+
+// ---- persistent per-rank level loop ------------------------------------------
+
+// One whole traversal of this rank inside the persistent megakernel
+// (megakernel.cuh, part = 1): levels, tree decisions and the fused exchange
+// (peer stores + mailbox wait) all on the device; one launch, one sync.
+static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const double *static24,
+                     int fixed_pair, int64_t chunk, abfs_level_record *recs,
+                     uint64_t *local_counts, size_t cap, size_t *n_levels) {
+    if (!p || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    if (!p->nranks) return fail(ABFS_EINVAL, "peers not set (abfs_part_set_peers / abfs_part_ipc_open)");
+    if (root < 0 || (uint64_t)root >= p->n)
+        return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
+                                     std::to_string(p->n));
+    ABFS_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    if (!p->mrecs) {
+        ABFS_CUDA(cudaMalloc(&p->q2, (p->n + 4) * 4));
+        ABFS_CUDA(cudaHostAlloc((void **)&p->mrecs, kMegaCapPart * sizeof(MegaRecord), cudaHostAllocMapped));
+        ABFS_CUDA(cudaHostGetDevicePointer((void **)&p->drecs, p->mrecs, 0));
+        ABFS_CUDA(cudaHostAlloc((void **)&p->mnlev, sizeof(unsigned long long), cudaHostAllocMapped));
+        ABFS_CUDA(cudaHostGetDevicePointer((void **)&p->dnlev, p->mnlev, 0));
+        ABFS_CUDA(cudaMalloc(&p->droots, 16));
+        ABFS_CUDA(cudaMalloc(&p->dx, 2 * sizeof(unsigned long long)));
+        ABFS_CUDA(cudaMemset(p->dx, 0, 2 * sizeof(unsigned long long)));
+    }
+    std::vector<unsigned char> blob;
+    uint32_t nn = 0;
+    stage_cut_tree(tr, static24, p->n, blob, nn);
+    if (blob.size() > p->tree_cap) {
+        cudaFree(p->dtree);
+        p->dtree = nullptr;
+        ABFS_CUDA(cudaMalloc(&p->dtree, blob.size()));
+        p->tree_cap = blob.size();
+    }
+    ABFS_CUDA(cudaMemcpy(p->dtree, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    const uint32_t r32 = (uint32_t)root;
+    ABFS_CUDA(cudaMemcpy(p->droots, &r32, 4, cudaMemcpyHostToDevice));
+    ABFS_CUDA(cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s));
+    ABFS_CUDA(cudaMemsetAsync(&p->box->timeout, 0, sizeof(unsigned int), s));
+    MegaParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.depth = p->depth - p->lo;
+    P.visited = p->visited - p->wlo;
+    P.noin = p->noin - p->wlo;
+    P.fbm0 = p->fbm[0];
+    P.fbm1 = p->fbm[1];
+    P.q0 = p->q;
+    P.q1 = p->q2;
+    P.units = p->units;
+    P.ctr = p->dctr;
+    P.out_off = p->fo_off;
+    P.dst = p->fo_dst;
+    P.org = p->fo_org;
+    P.in_off = p->r_off - p->lo;
+    P.src = p->r_src;
+    P.rev_owner = p->r_own;
+    P.first_src = p->r_first - p->lo;
+    P.n = p->n;
+    P.m = p->mf;
+    P.words = p->W;
+    P.tree = p->dtree;
+    P.tree_nodes = nn;
+    P.fixed_pair = fixed_pair;
+    P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
+    P.instrument = 0;
+    P.pull_light = kPullLight;
+    P.cap = kMegaCapPart;
+    P.recs = p->drecs;
+    P.n_levels = p->dnlev;
+    P.roots = p->droots;
+    P.nroots = 1;
+    P.init_in_kernel = 1;
+    P.solo_ctas = 0;
+    P.solo = nullptr;
+    P.part = 1;
+    P.m_rev = p->mr;
+    P.lo = p->lo;
+    P.hi = p->hi;
+    P.wlo = p->wlo;
+    P.wend = p->whi;
+    P.vprev = p->vprev;
+    P.fnext = p->fnext - p->wlo;
+    P.peer_fbm = p->peer_fbm;
+    P.peer_box = p->peer_box;
+    P.box = p->box;
+    P.nranks = p->nranks;
+    P.rank = p->rank;
+    P.xcount = p->dx;
+    P.gcount = p->dx + 1;
+    P.xseq0 = p->p2p_seq;
+    *(volatile unsigned long long *)p->mnlev = 0;
+    ABFS_CUDA(cudaEventRecord(p->e0, s));
+    ABFS_TRY(mega_launch_plain(P, s, p->device));
+    p->launches += 1;
+    ABFS_CUDA(cudaEventRecord(p->e1, s));
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long nl = *(volatile unsigned long long *)p->mnlev;
+    p->p2p_seq += nl;
+    p->last_kernel = -1;
+    p->has_q = false;
+    int timed_out = 0;
+    ABFS_CUDA(cudaMemcpy(&timed_out, &p->box->timeout, sizeof(int), cudaMemcpyDeviceToHost));
+    if (timed_out) return fail(ABFS_ENCCL, "peer exchange timed out (a rank never signalled a level)");
+    const size_t keep = nl < kMegaCapPart ? (size_t)nl : kMegaCapPart;
+    for (size_t l = 0; recs && l < keep && l < cap; ++l) {
+        const MegaRecord &m = p->mrecs[l];
+        abfs_level_record &r = recs[l];
+        r.level = (int64_t)l;
+        r.kernel = m.kernel;
+        r.variant = m.variant;
+        r.fallback = m.fallback;
+        r.converted = m.converted;
+        r.frontier_size = m.frontier;
+        r.new_count = m.new_count;
+        const uint64_t d = m.t_end > m.t_start ? m.t_end - m.t_start : 0;
+        r.elapsed_ns = d ? d : 1;
+        const uint64_t pn = m.t_pred > m.t_start ? m.t_pred - m.t_start : 0;
+        r.prediction_ns = pn ? pn : 1;
+    }
+    if (local_counts)
+        for (size_t l = 0; l < keep && l < cap; ++l) local_counts[l] = p->mrecs[l].scanned;
+    *n_levels = (size_t)nl;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_mega_adaptive_bfs(abfs_part *p, int64_t root, const abfs_tree *tree,
+                                           const double *static24, int64_t chunk_size,
+                                           abfs_level_record *records, uint64_t *local_counts,
+                                           size_t cap, size_t *n_levels) {
+    if (!tree || !static24) return fail(ABFS_EINVAL, "null argument");
+    ABFS_TRY(level_params_ok(0, 0, 0, chunk_size));
+    return part_mega(p, root, tree, static24, -1, chunk_size, records, local_counts, cap, n_levels);
+}
+
+extern "C" int abfs_part_mega_bfs_full(abfs_part *p, int64_t root, int kernel, int variant,
+                                       int64_t chunk_size, abfs_level_record *records,
+                                       uint64_t *local_counts, size_t cap, size_t *n_levels) {
+    ABFS_TRY(level_params_ok(0, kernel, variant, chunk_size));
+    return part_mega(p, root, nullptr, nullptr, kernel * 3 + variant, chunk_size, records,
+                     local_counts, cap, n_levels);
 }

@@ -282,6 +282,9 @@ class PartitionedBFS:
         # fused exchange over engine partitions: whole traversals run in C
         # (abfs_parts_*), no Python between levels
         self.native = self.fused and all(isinstance(p, DevicePartition) for p in self.parts)
+        # one partition per process (one per GPU): the whole per-rank level
+        # loop, exchange included, runs in one persistent kernel
+        self.persistent = self.native and len(self.parts) == 1
         self.stream = stream
         self.last_local_counts: list[list[int]] = []
         # optional: CUDA-event time of the all-gathers (bench NVLink figure)
@@ -327,16 +330,20 @@ class PartitionedBFS:
             p.init(root)
 
     # -- reference-shaped entry points ------------------------------------------
-    def _native_records(self, fn, *args):
+    def _native_records(self, fn, *args, single=False):
         cap = 1 << 16
         if getattr(self, "_native_buf", None) is None:
             self._native_buf = ((L.AbfsLevelRecord * cap)(),
                                 np.zeros(cap * len(self.parts), np.uint64))
         recs, loc = self._native_buf
         nl = ctypes.c_size_t()
-        handles = (ctypes.c_void_p * len(self.parts))(*[p._h.value for p in self.parts])
-        L.check(fn(handles, len(self.parts), *args, recs, L.ptr(loc, L.u64p), cap,
-                   ctypes.byref(nl)), fn.__name__)
+        if single:   # one partition per process: the persistent per-rank loop
+            L.check(fn(self.parts[0]._h, *args, recs, L.ptr(loc, L.u64p), cap, ctypes.byref(nl)),
+                    fn.__name__)
+        else:
+            handles = (ctypes.c_void_p * len(self.parts))(*[p._h.value for p in self.parts])
+            L.check(fn(handles, len(self.parts), *args, recs, L.ptr(loc, L.u64p), cap,
+                       ctypes.byref(nl)), fn.__name__)
         k = min(nl.value, cap)
         self.last_local_counts = loc[:k * len(self.parts)].reshape(k, len(self.parts)).tolist()
         return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:k]]
@@ -348,8 +355,12 @@ class PartitionedBFS:
         if self.native:
             if not 0 <= root < self.n:
                 raise ValueError(f"root {root} out of range for |V|={self.n}")
-            recs = self._native_records(L.lib().abfs_parts_bfs_full, int(root), int(kernel),
-                                        int(variant), int(chunk_size))
+            if self.persistent:
+                recs = self._native_records(L.lib().abfs_part_mega_bfs_full, int(root), int(kernel),
+                                            int(variant), int(chunk_size), single=True)
+            else:
+                recs = self._native_records(L.lib().abfs_parts_bfs_full, int(root), int(kernel),
+                                            int(variant), int(chunk_size))
             return [LevelOutcome(new_frontier_count=int(r.new_count), elapsed_ns=int(r.elapsed_ns))
                     for r in recs]
         self._init(root)
@@ -371,9 +382,14 @@ class PartitionedBFS:
                 raise ValueError(f"root {root} out of range for |V|={self.n}")
             from .features import static_vector
             st = np.ascontiguousarray(static_vector(stats), dtype=np.float64)
-            recs = self._native_records(L.lib().abfs_parts_adaptive_bfs, int(root),
-                                        ctypes.byref(model.as_abfs()), L.ptr(st, L.f64p),
-                                        int(chunk_size))
+            if self.persistent:
+                recs = self._native_records(L.lib().abfs_part_mega_adaptive_bfs, int(root),
+                                            ctypes.byref(model.as_abfs()), L.ptr(st, L.f64p),
+                                            int(chunk_size), single=True)
+            else:
+                recs = self._native_records(L.lib().abfs_parts_adaptive_bfs, int(root),
+                                            ctypes.byref(model.as_abfs()), L.ptr(st, L.f64p),
+                                            int(chunk_size))
             return AdaptiveTrace(tuple(
                 LevelTrace(level=int(r.level), kernel=KernelId(r.kernel),
                            variant=CountVariant(r.variant), fallback_used=bool(r.fallback),
