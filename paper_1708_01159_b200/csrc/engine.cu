@@ -730,7 +730,18 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         cfg.stream = s;
         cfg.attrs = at;
         cfg.numAttrs = 2;
-        ABFS_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
+        if (cudaLaunchKernelExC(&cfg, kfn, args) != cudaSuccess) {
+            // cluster + cooperative launch refused: plain cooperative launch
+            // without solo mode (same results, one grid barrier per level)
+            cudaGetLastError();
+            int per = 0, sms = 0;
+            ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
+            ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
+            t->mega_grid = per * sms;
+            t->mega_cluster = 0;
+            P.solo_ctas = 0;
+            ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
+        }
     } else {
         ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
     }
