@@ -8,8 +8,12 @@ from paper_1708_01159_b200 import DeviceGraph, Traversal
 from paper_1708_01159_b200.features import static_vector
 from bench import pick_roots
 KN = ["EDGE", "REV", "PUSH", "PULL", "PUSHW"]
-scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
-dg = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True)
+arg = sys.argv[1] if len(sys.argv) > 1 else "24"
+if arg == "er":
+    dg = DeviceGraph.uniform(1 << 25, 1 << 30, 1)
+else:
+    scale = int(arg)
+    dg = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True)
 oo, _ = dg.offsets()
 stats = P.compute_stats(dg)
 flat = P.deserialize("models/gpu_tree.tree")
