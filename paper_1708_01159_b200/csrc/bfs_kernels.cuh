@@ -774,6 +774,10 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // ---------------------------------------------------------------------------
 constexpr int kPullSub = 8;                  // words per sub-tile
 constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
+#ifndef ABFS_PROBE_BATCH
+#define ABFS_PROBE_BATCH 2
+#endif
+constexpr int kProbeBatch = ABFS_PROBE_BATCH;  // candidates per lane whose first probes are in flight together
 constexpr int kPullChunkSubs = 8;            // sub-tiles per CTA chunk fetch
 constexpr uint32_t kFetchInit = 0xfffffffeu, kFetchDone = 0xffffffffu;
 
@@ -862,16 +866,16 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 }
             }
             __syncwarp();
-            for (uint32_t base = 0; base < total; base += 64) {
+            for (uint32_t base = 0; base < total; base += 32 * kProbeBatch) {
                 // probe 0 for two candidates per lane at once: the offsets and
                 // the first in-neighbour (dense array, coalesced over
                 // consecutive candidates) of both, then both frontier bits --
                 // the smallest in-neighbour is a hub on skewed graphs, so
                 // most candidates stop here without touching src
-                uint32_t vv[2], jj[2], ee[2], ff0[2];
-                bool fnd[2];
+                uint32_t vv[kProbeBatch], jj[kProbeBatch], ee[kProbeBatch], ff0[kProbeBatch];
+                bool fnd[kProbeBatch];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < kProbeBatch; ++h) {
                     const bool has = base + h * 32 + lane < total;
                     vv[h] = has ? wbuf[base + h * 32 + lane] : 0u;
                     jj[h] = has ? __ldg(in_off + vv[h]) : 0u;
