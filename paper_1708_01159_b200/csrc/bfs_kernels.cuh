@@ -858,11 +858,15 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             const uint32_t total = __shfl_sync(kFull, incl, kPullSub - 1);
             if (!total) continue;
             {
-                uint32_t pos = incl - cnt, bits = cand;
-                while (bits) {
-                    const int b = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    wbuf[pos++] = myw * 32 + (uint32_t)b;
+                // all 32 lanes scatter one word at a time (lane l places bit
+                // l of word w): no serial per-bit loop on 8 divergent lanes
+                const uint32_t excl = incl - cnt;
+                const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int w = 0; w < kPullSub; ++w) {
+                    const uint32_t cw = __shfl_sync(kFull, cand, w);
+                    const uint32_t ow = __shfl_sync(kFull, excl, w);
+                    if ((cw >> lane) & 1u) wbuf[ow + __popc(cw & lt)] = (wbase + w) * 32 + lane;
                 }
             }
             __syncwarp();
