@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libabfs.so")
+# ABFS_LIB: an alternative build of the same library (A/B experiments, tools/)
+LIB_PATH = os.environ.get("ABFS_LIB") or os.path.join(_HERE, "libabfs.so")
 
 ABFS_OK, ABFS_EINVAL, ABFS_ECUDA, ABFS_ENCCL, ABFS_ENOMEM, ABFS_EFEATURE = range(6)
 

@@ -128,15 +128,43 @@ static_assert(sizeof(CutNode) == 32, "CutNode layout");
 
 constexpr uint32_t kMegaTreeNodes = 512;   // 16 KB of shared memory
 
+// The pruned tree is a pure function of (frontier, discovered): each leaf
+// owns a box [flo,fhi) x [dlo,dhi).  Thread 0 of a CTA keeps the box of its
+// last leaf (in shared memory: registers are the megakernel's scarcest
+// resource) and re-walks only when the counts leave it -- a mesh BFS stays in
+// one leaf for hundreds of levels, and a walk is a chain of dependent shared
+// loads (~0.5 us at depth 12).
+struct TreeCache {
+    unsigned long long flo, fhi, dlo, dhi;
+    int cls;
+};
+
 __device__ __forceinline__ int mega_tree_class(const CutNode *T, unsigned long long frontier,
-                                               unsigned long long discovered) {
+                                               unsigned long long discovered, TreeCache *tc) {
+    if (frontier >= tc->flo && frontier < tc->fhi && discovered >= tc->dlo && discovered < tc->dhi)
+        return tc->cls;
+    unsigned long long flo = 0, fhi = ~0ull, dlo = 0, dhi = ~0ull;
     uint32_t node = 0;
     while (T[node].cls == 255) {
         const CutNode &n = T[node];
         const unsigned long long x = n.on_disc ? discovered : frontier;
-        node = x < n.cutoff ? n.left : n.right;
+        const unsigned long long cut = n.cutoff;
+        if (x < cut) {
+            node = n.left;
+            if (n.on_disc) dhi = min(dhi, cut);
+            else fhi = min(fhi, cut);
+        } else {
+            node = n.right;
+            if (n.on_disc) dlo = max(dlo, cut);
+            else flo = max(flo, cut);
+        }
     }
-    return T[node].cls;
+    tc->flo = flo;
+    tc->fhi = fhi;
+    tc->dlo = dlo;
+    tc->dhi = dhi;
+    tc->cls = T[node].cls;
+    return tc->cls;
 }
 
 template <int VAR>
@@ -227,6 +255,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         T = s_tree;
     }
     __syncthreads();
+    __shared__ TreeCache tcache;   // thread 0's last leaf box
+    if (threadIdx.x == 0) tcache = TreeCache{1, 0, 1, 0, 0};   // empty box
     unsigned long long rec_off = 0;
     unsigned long long xseq = P.xseq0;   // fused exchanges so far (partition mode)
     for (uint32_t ri = 0; ri < P.nroots; ++ri) {
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     for (uint32_t level = 0;; ++level) {
         const unsigned long long t0 = lead ? globaltimer() : 0ull;
         if (threadIdx.x == 0)
-            s_cls = P.fixed_pair >= 0 ? P.fixed_pair : mega_tree_class(T, frontier, discovered);
+            s_cls = P.fixed_pair >= 0 ? P.fixed_pair : mega_tree_class(T, frontier, discovered, &tcache);
         __syncthreads();
         const int cls = s_cls;
         const int fallback = cls == 254;
@@ -397,7 +427,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                     ts = lead ? globaltimer() : 0ull;
                     if (threadIdx.x == 0)
                         s_cls = P.fixed_pair >= 0 ? P.fixed_pair
-                                                  : mega_tree_class(T, frontier, discovered);
+                                                  : mega_tree_class(T, frontier, discovered, &tcache);
                     __syncthreads();
                     const int ncls = s_cls;
                     fb = ncls == 254;

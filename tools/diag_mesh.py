@@ -26,3 +26,9 @@ print("switched median level", np.median(sw) / 1e3, "median prediction ns", np.m
 c, el = t.bfs_full(r, 4, 2)
 m = np.array([(x.kernel, x.variant) == (4, 2) for x in recs])
 print("PUSHW/2 levels in switched:", m.sum(), "switched", sw[m].sum() / 1e3, "fixed same levels", el[m].sum() / 1e3)
+# levels the tree ran as PUSH/GROUP vs the fixed PUSH/GROUP run, and the rest
+c, el = t.bfs_full(r, 2, 1)
+m = np.array([(x.kernel, x.variant) == (2, 1) for x in recs])
+print("PUSH/1 levels in switched:", m.sum(), "switched", sw[m].sum() / 1e3, "fixed same levels", el[m].sum() / 1e3,
+      "| other levels: switched", sw[~m].sum() / 1e3, "fixed PUSH/1", el[~m].sum() / 1e3,
+      "levels", np.flatnonzero(~m)[:20], "frontiers", [recs[i].frontier_size for i in np.flatnonzero(~m)[:20]])

@@ -103,6 +103,8 @@ def main():
     ap.add_argument("--max-levels", type=int, default=64)
     ap.add_argument("--menu", type=int, default=6,
                     help="restrict labels to a greedy menu of this many pairs (0 = all 15)")
+    ap.add_argument("--seed-menu", default="",
+                    help="comma list of pair ordinals the menu starts from")
     ap.add_argument("--grid", default="0,0.03,0.06,0.1/4,6,8,12/1,2,4",
                     help="quantisations / max depths / min leaf sizes to search")
     a = ap.parse_args()
@@ -144,7 +146,8 @@ def main():
             c_ = replay(fl, val_levels, table)
             r_ = [c_[k] / opt[k] for k in c_]
             return float(np.exp(np.mean(np.log(r_)))), max(r_)
-        menu, cur = [], None
+        menu = [int(x) for x in a.seed_menu.split(",") if x]
+        cur = menu_score(menu) if menu else None
         for _ in range(a.menu):
             cands = [(menu_score(menu + [p]), p) for p in range(15) if p not in menu]
             (sc, p) = min(cands, key=lambda z: (z[0][1] > 2.0, z[0][0]))
