@@ -287,10 +287,15 @@ struct QEmit {
 };
 
 // Count-only epilogue (pull): same three shapes over a warp's found mask.
+//   DIRECT    one global atomic per discovery
+//   GROUP     warp popc; the warp's sum goes out in one global atomic per
+//             sub-tile of work (tile())
+//   TWO_LEVEL warp popc -> CTA shared counter, one global atomic per CTA
 template <int VAR>
 struct CEmit {
     unsigned int *sn;
     unsigned long long *count;
+    unsigned acc = 0;   // GROUP: this warp's open sum (lane 0)
 
     __device__ __forceinline__ CEmit(unsigned int *smem_n, unsigned long long *c)
         : sn(smem_n), count(c) {
@@ -303,13 +308,22 @@ struct CEmit {
     __device__ __forceinline__ void add(unsigned mask) {  // warp-uniform mask
         if (VAR == 0) {
             if ((mask >> lane_id()) & 1u) atomicAdd(count, 1ull);
+        } else if (VAR == 1) {
+            acc += __popc(mask);
         } else if (mask && lane_id() == 0) {
-            if (VAR == 1) atomicAdd(count, (unsigned long long)__popc(mask));
-            else atomicAdd(sn, (unsigned)__popc(mask));
+            atomicAdd(sn, (unsigned)__popc(mask));
+        }
+    }
+
+    __device__ __forceinline__ void tile() {   // warp-uniform
+        if (VAR == 1 && acc) {
+            if (lane_id() == 0) atomicAdd(count, (unsigned long long)acc);
+            acc = 0;
         }
     }
 
     __device__ __forceinline__ void finish() {
+        tile();
         if (VAR != 2) return;
         __syncthreads();
         if (threadIdx.x == 0 && *sn) atomicAdd(count, (unsigned long long)*sn);
@@ -870,14 +884,17 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 }
             }
             __syncwarp();
+            // probe 0 for every candidate (two per lane at once): the offsets
+            // and the first in-neighbour (dense array, coalesced over
+            // consecutive candidates), then the frontier bits -- the smallest
+            // in-neighbour is a hub on skewed graphs, so most candidates stop
+            // here without touching src.  The rest are compacted in place to
+            // the front of wbuf, so the scans below run on full warps (a
+            // scan over the probe-0 survivors of a raw batch kept ~3 of 32
+            // lanes busy).
+            uint32_t npend = 0;
             for (uint32_t base = 0; base < total; base += 32 * kProbeBatch) {
-                // probe 0 for two candidates per lane at once: the offsets and
-                // the first in-neighbour (dense array, coalesced over
-                // consecutive candidates) of both, then both frontier bits --
-                // the smallest in-neighbour is a hub on skewed graphs, so
-                // most candidates stop here without touching src
                 uint32_t vv[kProbeBatch], jj[kProbeBatch], ee[kProbeBatch], ff0[kProbeBatch];
-                bool fnd[kProbeBatch];
 #pragma unroll
                 for (int h = 0; h < kProbeBatch; ++h) {
                     const bool has = base + h * 32 + lane < total;
@@ -886,25 +903,32 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                     ee[h] = has ? __ldg(in_off + vv[h] + 1) : 0u;
                     ff0[h] = has ? __ldg(first_src + vv[h]) : 0u;
                 }
+                __syncwarp();   // every lane has read its entries before the in-place writes
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    fnd[h] = false;
+                for (int h = 0; h < kProbeBatch; ++h) {
+                    bool found = false;
                     if (jj[h] < ee[h]) {
                         ++scanned;
-                        if (in_bitmap(c.fbm, ff0[h])) {
-                            fnd[h] = true;
-                            jj[h] = ee[h];
-                        } else {
-                            ++jj[h];
-                        }
+                        found = in_bitmap(c.fbm, ff0[h]);
                     }
+                    if (found) {
+                        c.depth[vv[h]] = c.lvl1;
+                        atomicOr(wfound + ((vv[h] >> 5) - wbase), 1u << (vv[h] & 31));
+                    }
+                    em.add(__ballot_sync(kFull, found));
+                    const bool pend = !found && jj[h] + 1 < ee[h];
+                    const unsigned pm = __ballot_sync(kFull, pend);
+                    if (pend) wbuf[npend + __popc(pm & ((1u << lane) - 1u))] = vv[h];
+                    npend += __popc(pm);
                 }
-              for (int h = 0; h < 2; ++h) {
-                if (base + h * 32 >= total) break;   // warp-uniform
-                const uint32_t v = vv[h];
-                uint32_t j = jj[h];
-                const uint32_t e = ee[h];
-                bool found = fnd[h];
+            }
+            __syncwarp();
+            for (uint32_t base = 0; base < npend; base += 32) {
+                const bool has = base + lane < npend;
+                const uint32_t v = has ? wbuf[base + lane] : 0u;
+                uint32_t j = has ? __ldg(in_off + v) + 1 : 0u;   // L1 hits: just probed
+                const uint32_t e = has ? __ldg(in_off + v + 1) : 0u;
+                bool found = false;
                 // phase A: each candidate scans up to pull_light more of its
                 // in-neighbours, one aligned 16-byte load per step (one L1
                 // wavefront per lane instead of four), early exit
@@ -980,8 +1004,8 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                     atomicOr(wfound + ((v >> 5) - wbase), 1u << (v & 31));
                 }
                 em.add(__ballot_sync(kFull, found));
-              }
             }
+            em.tile();
             __syncwarp();
             if (mine && cand) {
                 const uint32_t fm = wfound[lane];
