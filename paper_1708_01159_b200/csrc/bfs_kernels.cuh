@@ -290,12 +290,13 @@ struct QEmit {
 //   DIRECT    one global atomic per discovery
 //   GROUP     warp popc; the warp's sum goes out in one global atomic per
 //             sub-tile of work (tile())
-//   TWO_LEVEL warp popc -> CTA shared counter, one global atomic per CTA
+//   TWO_LEVEL warp popc -> CTA shared counter (one shared atomic per warp
+//             sub-tile), one global atomic per CTA
 template <int VAR>
 struct CEmit {
     unsigned int *sn;
     unsigned long long *count;
-    unsigned acc = 0;   // GROUP: this warp's open sum (lane 0)
+    unsigned acc = 0;   // GROUP / TWO_LEVEL: this warp's open sum
 
     __device__ __forceinline__ CEmit(unsigned int *smem_n, unsigned long long *c)
         : sn(smem_n), count(c) {
@@ -308,16 +309,17 @@ struct CEmit {
     __device__ __forceinline__ void add(unsigned mask) {  // warp-uniform mask
         if (VAR == 0) {
             if ((mask >> lane_id()) & 1u) atomicAdd(count, 1ull);
-        } else if (VAR == 1) {
+        } else {
             acc += __popc(mask);
-        } else if (mask && lane_id() == 0) {
-            atomicAdd(sn, (unsigned)__popc(mask));
         }
     }
 
     __device__ __forceinline__ void tile() {   // warp-uniform
-        if (VAR == 1 && acc) {
-            if (lane_id() == 0) atomicAdd(count, (unsigned long long)acc);
+        if (VAR != 0 && acc) {
+            if (lane_id() == 0) {
+                if (VAR == 1) atomicAdd(count, (unsigned long long)acc);
+                else atomicAdd(sn, acc);
+            }
             acc = 0;
         }
     }
@@ -793,7 +795,9 @@ constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
 #endif
 constexpr int kProbeBatch = ABFS_PROBE_BATCH;  // candidates per lane whose first probes are in flight together
 constexpr int kPullChunkSubs = 8;            // sub-tiles per CTA chunk fetch
-constexpr uint32_t kFetchInit = 0xfffffffeu, kFetchDone = 0xffffffffu;
+// CTA chunk cursor: one 32-bit shared word (chunk id << 8 | next sub-tile),
+// so the fetch is a native shared atomic (a 64-bit one is a CAS loop)
+constexpr uint32_t kFetchInit = 0xfffffeu, kFetchDone = 0xffffffu;
 
 template <int VAR>
 __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
@@ -803,7 +807,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ noin,
                                           uint32_t *__restrict__ fbm_next, uint64_t word0,
                                           uint64_t words, uint32_t *wbuf, uint32_t *wfound,
-                                          unsigned long long *sfetch) {
+                                          unsigned int *sfetch) {
     // words [word0, words) of the bitmaps (a vertex partition passes its
     // owned range; bitmap/offset pointers are indexed by global ids);
     // wbuf = kPullList entries, wfound = kPullSub words, both per warp
@@ -820,18 +824,18 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
     const uint32_t w0 = (uint32_t)word0, wend = (uint32_t)words;
     const uint32_t nsub = (wend - w0 + kPullSub - 1) / kPullSub;
     const uint32_t nchunks = (nsub + kPullChunkSubs - 1) / kPullChunkSubs;
-    if (threadIdx.x == 0) *sfetch = ((unsigned long long)kFetchInit << 32) | kPullChunkSubs;
+    if (threadIdx.x == 0) *sfetch = (kFetchInit << 8) | kPullChunkSubs;
     __syncthreads();
     unsigned long long scanned = 0;
     for (;;) {
-        unsigned long long st = 0;
-        if (lane == 0) st = atomicAdd(sfetch, 1ull);
+        uint32_t st = 0;
+        if (lane == 0) st = atomicAdd(sfetch, 1u);
         st = __shfl_sync(kFull, st, 0);
-        uint32_t cid = (uint32_t)(st >> 32), sidx = (uint32_t)st;
+        uint32_t cid = st >> 8, sidx = st & 0xffu;
         if (cid == kFetchDone) break;
         if (sidx > (uint32_t)kPullChunkSubs) {   // another warp is refilling the chunk
             if (lane == 0)
-                while ((uint32_t)(*(volatile unsigned long long *)sfetch >> 32) == cid) {
+                while ((*(volatile unsigned int *)sfetch >> 8) == cid) {
                 }
             __syncwarp();
             continue;
@@ -840,8 +844,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             unsigned long long g = 0;
             if (lane == 0) {
                 g = atomicAdd(c.work, 1ull);
-                atomicExch(sfetch, g < nchunks ? (g << 32) | 1ull
-                                               : (unsigned long long)kFetchDone << 32);
+                atomicExch(sfetch, g < nchunks ? ((uint32_t)g << 8) | 1u : kFetchDone << 8);
             }
             g = __shfl_sync(kFull, g, 0);
             if (g >= nchunks) break;
@@ -1036,7 +1039,7 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
        uint32_t *__restrict__ fbm_next, uint64_t word0, uint64_t words) {
     __shared__ unsigned int sn;
     __shared__ SmemPull sp;
-    __shared__ unsigned long long sfetch;
+    __shared__ unsigned int sfetch;
     zero_slot(c);
     const unsigned w = threadIdx.x >> 5;
     pull_body<VAR>(c, &sn, in_off, src, first_src, noin, fbm_next, word0, words, sp.list[w],

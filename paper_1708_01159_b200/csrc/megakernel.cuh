@@ -171,7 +171,7 @@ template <int VAR>
 __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
                                               uint32_t F, const uint32_t *q, uint32_t *fbm_next,
                                               SmemQ *sq, unsigned *sn, int *s_done,
-                                              uint32_t *pfound, unsigned long long *sfetch,
+                                              uint32_t *pfound, unsigned int *sfetch,
                                               cg::grid_group &grid) {
     // Two-phase strategies (light pass, then CTA work units) need a second
     // barrier only if the light pass created units: after the first barrier
@@ -236,7 +236,7 @@ template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
     __shared__ uint32_t pfound[kWarps * kPullSub];
-    __shared__ unsigned long long s_fetch;
+    __shared__ unsigned int s_fetch;
     __shared__ unsigned sn;
     __shared__ int s_done;
     __shared__ int s_cls;
