@@ -207,6 +207,19 @@ __device__ __forceinline__ void claim4(const LevelCtx &c, const uint32_t (&v)[4]
 // emit() must be called by all 32 lanes of a warp together; tile_end() and
 // finish() by all threads of the CTA.
 // ---------------------------------------------------------------------------
+// Single-lane atomics without the compiler's warp-aggregation wrapper.
+__device__ __forceinline__ unsigned atom_add_shared(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                 : "=r"(old) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned atom_add_global(unsigned *p, unsigned v) {   // generic address
+    unsigned old;
+    asm volatile("atom.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 struct SmemQ {
     unsigned int n;
     unsigned int fail;
@@ -241,13 +254,13 @@ struct QEmit {
         const unsigned rank = __popc(mask & ((1u << lane) - 1u));
         if (VAR == 1) {
             unsigned b = 0;
-            if (lane == (unsigned)leader) b = atomicAdd(tail, cnt);
+            if (lane == (unsigned)leader) b = atom_add_global(tail, cnt);
             b = __shfl_sync(kFull, b, leader);
             if (won) q[b + rank] = v;
             return;
         }
         unsigned sb = 0;
-        if (lane == (unsigned)leader) sb = atomicAdd(&s->n, cnt);
+        if (lane == (unsigned)leader) sb = atom_add_shared(&s->n, cnt);
         sb = __shfl_sync(kFull, sb, leader);
         if (sb + cnt <= (unsigned)kQBuf) {
             if (won) s->buf[sb + rank] = v;
@@ -255,10 +268,56 @@ struct QEmit {
             unsigned b = 0;
             if (lane == (unsigned)leader) {
                 atomicMin(&s->fail, sb);
-                b = atomicAdd(tail, cnt);
+                b = atom_add_global(tail, cnt);
             }
             b = __shfl_sync(kFull, b, leader);
             if (won) q[b + rank] = v;
+        }
+    }
+
+    // Four candidates per lane (a claim4 step) with ONE reservation for all
+    // of the warp's winners: one atomic per step instead of up to four, and
+    // the reservation is issued by lane 0 as a plain atom (the compiler's own
+    // warp-aggregation wrapper around a leader-lane atomicAdd costs ~15
+    // single-thread instructions per call).
+    __device__ __forceinline__ void emit4(const bool (&won)[4], const uint32_t (&v)[4]) {
+        if (VAR == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) emit(won[k], v[k]);
+            return;
+        }
+        unsigned m[4], tot = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            m[k] = __ballot_sync(kFull, won[k]);
+            tot += __popc(m[k]);
+        }
+        if (!tot) return;
+        const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
+        unsigned base = 0;
+        bool to_global = VAR == 1;
+        if (VAR == 2) {
+            if (lane == 0) base = atom_add_shared(&s->n, tot);
+            base = __shfl_sync(kFull, base, 0);
+            if (base + tot <= (unsigned)kQBuf) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (won[k]) s->buf[base + __popc(m[k] & lt)] = v[k];
+                    base += __popc(m[k]);
+                }
+                return;
+            }
+            if (lane == 0) atomicMin(&s->fail, base);   // CTA buffer full: straight to global
+            to_global = true;
+        }
+        if (to_global) {
+            if (lane == 0) base = atom_add_global(tail, tot);
+            base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (won[k]) q[base + __popc(m[k] & lt)] = v[k];
+                base += __popc(m[k]);
+            }
         }
     }
 
@@ -645,8 +704,7 @@ __device__ __forceinline__ void push_body(const LevelCtx &c, SmemQ *sq,
             }
             j = min(e, j + 4);
             claim4(c, v, act, won, consistent);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
+            em.emit4(won, v);
         }
         em.tile_end();
     }
@@ -711,8 +769,7 @@ __device__ __forceinline__ void push_warp_body(const LevelCtx &c, SmemQ *sq,
             }
             j += 4 * VW;
             claim4(c, v, act, won, consistent);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
+            em.emit4(won, v);
         }
         em.tile_end();
     }
@@ -753,8 +810,7 @@ __device__ __forceinline__ void heavy_body(const LevelCtx &c, SmemQ *sq,
                 v[k] = act[k] ? __ldg(dst + j) : 0u;
             }
             claim4(c, v, act, won, consistent);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) em.emit(won[k], v[k]);
+            em.emit4(won, v);
         }
         em.tile_end();
     }
