@@ -377,7 +377,7 @@ struct CEmit {
         if (VAR != 0 && acc) {
             if (lane_id() == 0) {
                 if (VAR == 1) atomicAdd(count, (unsigned long long)acc);
-                else atomicAdd(sn, acc);
+                else atom_add_shared(sn, acc);
             }
             acc = 0;
         }
@@ -885,7 +885,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
     unsigned long long scanned = 0;
     for (;;) {
         uint32_t st = 0;
-        if (lane == 0) st = atomicAdd(sfetch, 1u);
+        if (lane == 0) st = atom_add_shared(sfetch, 1u);
         st = __shfl_sync(kFull, st, 0);
         uint32_t cid = st >> 8, sidx = st & 0xffu;
         if (cid == kFetchDone) break;
