@@ -94,7 +94,10 @@ struct LevelCtx {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kQBuf = 2048;           // TWO_LEVEL CTA-local queue buffer
+#ifndef ABFS_QBUF
+#define ABFS_QBUF 2048
+#endif
+constexpr int kQBuf = ABFS_QBUF;      // TWO_LEVEL CTA-local queue buffer (also the megakernel's pull lists)
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 256;      // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 1024;      // edges per CTA work unit (4 steps of 256)
@@ -844,7 +847,10 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // next-frontier words, so they are written without global atomics, and every
 // next-frontier word is written (no clearing pass).
 // ---------------------------------------------------------------------------
-constexpr int kPullSub = 8;                  // words per sub-tile
+#ifndef ABFS_PULL_SUB
+#define ABFS_PULL_SUB 8
+#endif
+constexpr int kPullSub = ABFS_PULL_SUB;      // words per sub-tile
 constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
 #ifndef ABFS_PROBE_BATCH
 #define ABFS_PROBE_BATCH 2
