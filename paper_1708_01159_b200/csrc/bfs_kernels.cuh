@@ -831,14 +831,17 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 // ---------------------------------------------------------------------------
 // VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): unvisited
 // vertices scan their in-neighbours and stop at the first frontier vertex.
-// A warp takes a tile of 32 bitmap words (one atomic fetch) and walks it in
-// sub-tiles of 8 words (256 vertices).  Fully settled words (visited or
-// in-degree 0) cost one load and one store.  The candidates of a sub-tile
-// (unvisited, in-degree > 0) are compacted into a per-warp shared-memory
-// list, then processed 32 at a time, one lane per candidate, so every lane
-// carries a real vertex (a word with 3 candidates no longer idles 29 lanes
-// through a chain of dependent loads):
-//   first pull_light entries  each lane scans its own list, 4 loads in flight
+// The CTA takes chunks of 8 sub-tiles (one global atomic), its warps take
+// sub-tiles of 8 words (256 vertices) from a shared cursor.  Fully settled
+// words (visited or in-degree 0) cost one load and one store.  The
+// candidates of a sub-tile (unvisited, in-degree > 0) are compacted into a
+// per-warp shared-memory list, so every lane carries a real vertex (a word
+// with 3 candidates no longer idles 29 lanes through a chain of dependent
+// loads):
+//   probe 0                   two candidates per lane, first in-neighbour
+//                             from the dense first_src array
+//   survivors, compacted again in place, 32 per step:
+//   first pull_light entries  each lane scans its own list, 16-byte loads
 //   rest <= kPullHeavy        the warp scans the pending remainders together,
 //                             128 entries per step (load balanced)
 //   rest larger               kUnit-edge CTA units (k_pull_heavy)
