@@ -859,7 +859,10 @@ constexpr int kPullList = kPullSub * 32;     // candidate list entries per warp
 #define ABFS_PROBE_BATCH 2
 #endif
 constexpr int kProbeBatch = ABFS_PROBE_BATCH;  // candidates per lane whose first probes are in flight together
-constexpr int kPullChunkSubs = 8;            // sub-tiles per CTA chunk fetch
+#ifndef ABFS_PULL_CHUNK
+#define ABFS_PULL_CHUNK 8
+#endif
+constexpr int kPullChunkSubs = ABFS_PULL_CHUNK;  // sub-tiles per CTA chunk fetch
 // CTA chunk cursor: one 32-bit shared word (chunk id << 8 | next sub-tile),
 // so the fetch is a native shared atomic (a 64-bit one is a CAS loop)
 constexpr uint32_t kFetchInit = 0xfffffeu, kFetchDone = 0xffffffu;
