@@ -274,7 +274,11 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
     t->words = (n + 31) / 32;
     const uint64_t wpad = t->words + 4;
     const uint64_t qcap = n + 4;
-    const uint64_t ucap = m / kHeavy + 64;   // units of both heavy paths (<= deg/kHeavy each)
+    // CTA work units of one level: a vertex-push hub (degree > kPushHub)
+    // yields ceil(deg / kUnit) <= deg / kPushHub units, a push-warp hub or a
+    // pull remainder (> kHeavy / kPullHeavy) fewer -- m / kPushHub bounds all
+    const uint64_t ucap = m / kPushHub + 64;
+    static_assert(kPushHub <= kHeavy && kPushHub <= kPullHeavy && kPushHub <= kUnit, "unit bound");
     cudaError_t e = cudaSuccess;
     auto A = [&](void **p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);

@@ -385,7 +385,7 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     A((void **)&p->q, (n + 4) * 4);
     A((void **)&p->qn, (p->nv + 4) * 4);
     const uint64_t mx = p->mf > p->mr ? p->mf : p->mr;
-    A((void **)&p->units, (mx / kHeavy + 64) * sizeof(uint2));
+    A((void **)&p->units, (mx / kPushHub + 64) * sizeof(uint2));   // see traversal ucap
     A((void **)&p->dctr, sizeof(Ctr));
     A((void **)&p->dmb, sizeof(Mailbox));
     A((void **)&p->dres, 2 * sizeof(unsigned long long));

@@ -196,6 +196,29 @@ def test_larger_random_graphs_vs_oracle():
                     for r in tr.records] == [(k_, v_, fb, fr) for (_, k_, v_, fb, fr, *_x) in orecs]
 
 
+def test_push_level_of_mid_degree_hubs():
+    """A push level whose frontier is thousands of vertices of degree 65..255
+    (each one CTA work unit: more units than m / kHeavy) -- the unit buffer
+    is sized for m / kPushHub.  Both level drivers, all variants."""
+    rng = np.random.default_rng(7)
+    n = 4096
+    half = np.stack([np.repeat(np.arange(n), 50), rng.integers(0, n, n * 50)], axis=1)
+    g = P.build_combined(np.concatenate([half, half[:, ::-1]]), n)
+    deg = np.diff(np.asarray(g.out_offsets, dtype=np.int64))
+    assert deg.min() > 64 and deg.max() < 256
+    og = oracle.OracleGraph.from_graph(g)
+    for root in (0, 1234):
+        want = oracle.reference_bfs(og, root)
+        for k in (P.KernelId.VERTEX_PUSH, P.KernelId.VERTEX_PUSH_WARP):
+            for v in P.CountVariant:
+                d, outs = P.bfs_full(g, root, k, v)
+                np.testing.assert_array_equal(d, want)
+                t = P.Traversal(P.DeviceGraph.upload(g))
+                t.set_device_loop(0)
+                counts, _ = t.bfs_full(root, int(k), int(v))
+                assert counts.tolist() == [o.new_frontier_count for o in outs]
+
+
 @pytest.mark.parametrize("name", ["kron12", "er12", "mesh64", "u1000", "path9", "star7"])
 def test_device_loop_and_launch_loop_agree(name):
     """The persistent megakernel (default) and the per-level launch chain give
