@@ -342,8 +342,10 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     if (e == cudaSuccess) e = cudaMemcpyAsync(&mf, p->fo_off + n, 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     p->mf = mf;
-    A((void **)&p->fo_dst, (uint64_t)mf * 4);
-    A((void **)&p->fo_org, (uint64_t)mf * 4);
+    // +16 on every stream array: the edge kernels' bulk copies move whole
+    // 16-byte groups (chunk_bytes rounds the last chunk up)
+    A((void **)&p->fo_dst, (uint64_t)mf * 4 + 16);
+    A((void **)&p->fo_org, (uint64_t)mf * 4 + 16);
     if (e == cudaSuccess && m) {
         k_part_fcopy<<<148 * 16, kBlock, 0, s>>>(g->d.org, g->d.dst, m, start, p->fo_off, (uint32_t)lo,
                                                  (uint32_t)hi, p->fo_dst, p->fo_org);
@@ -360,7 +362,7 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     p->mr = (uint64_t)re - rb;
     A((void **)&p->r_off, (p->nv + 1) * 4);
     A((void **)&p->r_src, p->mr * 4 + 16);   // +16: aligned 16-byte reads in pull
-    A((void **)&p->r_own, p->mr * 4);
+    A((void **)&p->r_own, p->mr * 4 + 16);
     A((void **)&p->r_first, p->nv * 4 + 16);
     if (e == cudaSuccess && p->nv)
         e = cudaMemcpyAsync(p->r_first, g->d.first_src + lo, p->nv * 4, cudaMemcpyDeviceToDevice, s);
