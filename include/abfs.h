@@ -176,6 +176,18 @@ ABFS_API int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, si
                                      const abfs_tree *tree, const double *static24,
                                      int64_t chunk_size, uint64_t *levels, uint64_t *bfs_ns,
                                      uint64_t *total_ns);
+/* The same batch with per-root parity evidence (tests; not on the timed
+ * path): checksums[i] = sum over v of (uint64(uint32(depth_i[v])) + 1) *
+ * ((v + 1) * 0x9E3779B97F4A7C15) mod 2^64 of root i's final depth array,
+ * computed in the kernel after each traversal; new_counts = every root's
+ * per-level new counts concatenated (root order, levels[i] each; the first
+ * counts_cap are written, *n_counts = how many the launch recorded). */
+ABFS_API int abfs_adaptive_bfs_batch_check(abfs_traversal *t, const int64_t *roots,
+                                           size_t nroots, const abfs_tree *tree,
+                                           const double *static24, int64_t chunk_size,
+                                           uint64_t *levels, uint64_t *checksums,
+                                           uint64_t *new_counts, size_t counts_cap,
+                                           size_t *n_counts);
 
 /* Total device time (ns) of the last abfs_bfs_full/abfs_adaptive_bfs call,
  * from after init_depths to the final count readback. */
@@ -292,6 +304,38 @@ ABFS_API int abfs_part_mega_bfs_full(abfs_part *p, int64_t root, int kernel, int
 ABFS_API int abfs_part_read_depths(abfs_part *p, int32_t *host_owned);
 ABFS_API int abfs_part_depths_device(abfs_part *p, int32_t *dev_out);
 ABFS_API int abfs_part_launches(const abfs_part *p, uint64_t *launches);
+
+/* ---- reference artefacts on the engine side -------------- */
+/* With these a C/C++ host runs a tree-switched BFS from the reference's own
+ * files without Python: abfs_graph_read -> abfs_traversal_create ->
+ * abfs_tree_read -> abfs_adaptive_bfs -> abfs_trace_write. */
+
+/* read_graph (graph.py:304-324): ADGR file streamed straight into HBM;
+ * ABFS_EINVAL with the reference's ValueError texts (bad magic / truncated
+ * header / unsupported version / truncated file / trailing bytes). */
+ABFS_API int abfs_graph_read(int device, const char *path, abfs_graph **out);
+/* write_graph (graph.py:292-301): byte-identical ADGR file. */
+ABFS_API int abfs_graph_write(const abfs_graph *g, const char *path);
+
+/* deserialize (tree.py:409-447): an ADBT model; the selection names are
+ * resolved to canonical feature indices (validate_selection,
+ * features.py:53-63).  abfs_tree_file_view gives the abfs_tree the traversal
+ * calls take; valid until abfs_tree_file_free. */
+typedef struct abfs_tree_file abfs_tree_file;
+ABFS_API int abfs_tree_read(const char *path, abfs_tree_file **out);
+ABFS_API const abfs_tree *abfs_tree_file_view(const abfs_tree_file *t);
+ABFS_API void abfs_tree_file_free(abfs_tree_file *t);
+/* serialize (tree.py:389-406): byte-identical ADBT file (selection written
+ * as the canonical names of tree->selection). */
+ABFS_API int abfs_tree_write(const abfs_tree *tree, const char *path);
+
+/* write_trace / read_trace (adaptive.py:225-254): the trace CSV, byte-
+ * identical to Python's csv writer ("\r\n" line ends).  read: up to cap
+ * records into recs (NULL to count), *n = rows in the file; new_count and
+ * converted are not CSV columns and read back as 0. */
+ABFS_API int abfs_trace_write(const char *path, const abfs_level_record *records, size_t n);
+ABFS_API int abfs_trace_read(const char *path, abfs_level_record *records, size_t cap,
+                             size_t *n);
 
 /* ---- helpers ------------------------------------------------------------ */
 

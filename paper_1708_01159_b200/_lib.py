@@ -56,6 +56,16 @@ _SIGNATURES = {
     "abfs_graph_generate_uniform": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                                    u64p, u64p, vpp]),
     "abfs_graph_generate_mesh": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, vpp]),
+    "abfs_graph_read": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, vpp]),
+    "abfs_graph_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "abfs_tree_read": (ctypes.c_int, [ctypes.c_char_p, vpp]),
+    "abfs_tree_file_view": (ctypes.POINTER(AbfsTree), [ctypes.c_void_p]),
+    "abfs_tree_file_free": (None, [ctypes.c_void_p]),
+    "abfs_tree_write": (ctypes.c_int, [ctypes.POINTER(AbfsTree), ctypes.c_char_p]),
+    "abfs_trace_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(AbfsLevelRecord),
+                                        ctypes.c_size_t]),
+    "abfs_trace_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(AbfsLevelRecord),
+                                       ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "abfs_graph_info": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p, ctypes.POINTER(ctypes.c_int)]),
     "abfs_graph_download": (ctypes.c_int, [ctypes.c_void_p, u32p, u32p, u32p, u32p, u32p, u32p]),
     "abfs_graph_destroy": (None, [ctypes.c_void_p]),
@@ -79,6 +89,10 @@ _SIGNATURES = {
     "abfs_adaptive_bfs_batch": (ctypes.c_int, [ctypes.c_void_p, i64p, ctypes.c_size_t,
                                                ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
                                                u64p, u64p, u64p]),
+    "abfs_adaptive_bfs_batch_check": (ctypes.c_int, [ctypes.c_void_p, i64p, ctypes.c_size_t,
+                                                     ctypes.POINTER(AbfsTree), f64p, ctypes.c_int64,
+                                                     u64p, u64p, u64p, ctypes.c_size_t,
+                                                     ctypes.POINTER(ctypes.c_size_t)]),
     "abfs_last_traversal_ns": (ctypes.c_int, [ctypes.c_void_p, u64p]),
     "abfs_traversal_set_mode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "abfs_traversal_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),

@@ -1028,7 +1028,9 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                 if (pend && e - j > kPullHeavy) {
                     const uint32_t nu = (e - j + kUnit - 1) / kUnit;
                     const uint32_t s = atomicAdd(c.units_tail, nu);
-                    for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(v, k);
+                    // a unit carries its absolute start slot: the units cover
+                    // exactly the unscanned remainder [j, e)
+                    for (uint32_t k = 0; k < nu; ++k) c.units[s + k] = make_uint2(v, j + k * kUnit);
                     pend = false;
                 }
                 // phase B: the warp walks the concatenation of all pending
@@ -1115,7 +1117,8 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
-// segment of one vertex's in-list with early exit; the first unit to find a
+// segment [un.y, un.y + kUnit) of one vertex's unscanned in-list remainder
+// with early exit; the first unit to find a
 // frontier in-neighbour claims the vertex (atomicOr on its visited bit).
 __device__ __forceinline__ void pull_heavy_body(const LevelCtx &c, int *s_done_p,
                                                 const uint32_t *__restrict__ in_off,
@@ -1126,7 +1129,7 @@ __device__ __forceinline__ void pull_heavy_body(const LevelCtx &c, int *s_done_p
     for (unsigned w = blockIdx.x; w < nunits; w += gridDim.x) {
         const uint2 un = c.units[w];
         const uint32_t v = un.x, bit = 1u << (v & 31);
-        const uint32_t b = __ldg(in_off + v) + un.y * kUnit;
+        const uint32_t b = un.y;   // absolute start slot of this unit
         const uint32_t e = min(__ldg(in_off + v + 1), b + kUnit);
         if (threadIdx.x == 0) s_done = (*(volatile uint32_t *)(c.visited + (v >> 5)) & bit) ? 1 : 0;
         __syncthreads();

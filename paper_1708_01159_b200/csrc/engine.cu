@@ -14,6 +14,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,10 @@ static uint64_t host_ns() {
 using namespace abfs;
 
 struct abfs_traversal {
+    // per-handle lock: calls on one traversal are serialised,
+    // distinct traversals of one graph run concurrently;
+    // recursive because entry points call each other (run_level -> load/read)
+    mutable std::recursive_mutex mu;
     abfs_graph *g = nullptr;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -71,6 +76,7 @@ struct abfs_traversal {
     std::vector<MegaRecord> hrecs;
     unsigned long long *mnlev = nullptr, *dnlev = nullptr;   // host-mapped level counts (per root)
     uint32_t *hroots = nullptr, *droots = nullptr;            // batch roots (pinned / device)
+    unsigned long long *dsums = nullptr;                     // per-root depth checksums (device)
     std::vector<unsigned char> last_blob;                    // tree blob resident on the device
     std::vector<unsigned long long> batch_levels;            // per-root level counts, last launch
     size_t batch_recs = 0;                                   // records kept in mrecs, last launch
@@ -84,6 +90,16 @@ struct abfs_traversal {
     char *stage = nullptr;                     // pinned D2H staging (2 chunks)
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
+
+#define ABFS_LOCK(t) std::lock_guard<std::recursive_mutex> _abfs_guard((t)->mu)
+
+// Cooperative megakernels of one device run one at a time: two persistent
+// grids sharing the SMs could each be partly resident and wait at a grid
+// barrier for blocks that never get scheduled.
+static std::mutex g_mega_mu[64];
+namespace abfs {
+std::mutex &mega_mutex(int device) { return g_mega_mu[device & 63]; }
+}  // namespace abfs
 
 extern "C" const char *abfs_last_error(void) { return g_err.c_str(); }
 extern "C" int abfs_version(void) { return 1; }
@@ -329,6 +345,7 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
 
 extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     if (!t) return;
+    { ABFS_LOCK(t); }   // no call on this handle is in flight any more
     cudaSetDevice(t->device);
     if (t->stream) cudaStreamSynchronize(t->stream);
     cudaFree(t->depth);
@@ -346,6 +363,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     if (t->mnlev) cudaFreeHost(t->mnlev);
     if (t->hroots) cudaFreeHost(t->hroots);
     cudaFree(t->droots);
+    cudaFree(t->dsums);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
     if (t->stage) cudaFreeHost(t->stage);
@@ -361,6 +379,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
 
 extern "C" int abfs_traversal_set_stream(abfs_traversal *t, void *stream) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_LOCK(t);
     ABFS_CUDA(cudaSetDevice(t->device));
     ABFS_CUDA(cudaStreamSynchronize(t->stream));
     if (t->own_stream) cudaStreamDestroy(t->stream);
@@ -396,6 +415,7 @@ static int init_impl(abfs_traversal *t, int64_t root) {
 
 extern "C" int abfs_init_depths(abfs_traversal *t, int64_t root) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_LOCK(t);
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaStreamSynchronize(t->stream));
     return ABFS_OK;
@@ -403,6 +423,7 @@ extern "C" int abfs_init_depths(abfs_traversal *t, int64_t root) {
 
 extern "C" int abfs_load_depths(abfs_traversal *t, const int32_t *host) {
     if (!t || !host) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_CUDA(cudaSetDevice(t->device));
     ABFS_CUDA(cudaMemcpyAsync(t->depth, host, t->g->d.n * sizeof(int32_t),
                               cudaMemcpyHostToDevice, t->stream));
@@ -418,6 +439,7 @@ constexpr size_t kStageChunk = 8u << 20;   // bytes
 
 extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
     if (!t || !host) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_CUDA(cudaSetDevice(t->device));
     const size_t bytes = t->g->d.n * sizeof(int32_t);
     cudaPointerAttributes pa;
@@ -462,6 +484,7 @@ extern "C" int abfs_read_depths(abfs_traversal *t, int32_t *host) {
 extern "C" int abfs_level(abfs_traversal *t, int64_t level, int kernel, int variant,
                           int64_t chunk, uint64_t *new_count, uint64_t *elapsed_ns) {
     if (!t || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     return level_impl(t, level, kernel, variant, chunk, new_count, 0, true, elapsed_ns, nullptr);
 }
 
@@ -469,6 +492,7 @@ extern "C" int abfs_run_level(abfs_traversal *t, int32_t *host, int64_t level, i
                               int variant, int64_t chunk, uint64_t *new_count,
                               uint64_t *elapsed_ns) {
     if (!t || !host || !new_count || !elapsed_ns) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_TRY(level_params_ok(level, kernel, variant, chunk));
     ABFS_TRY(abfs_load_depths(t, host));
     ABFS_TRY(level_impl(t, level, kernel, variant, chunk, new_count, 0, true, elapsed_ns, nullptr));
@@ -562,7 +586,11 @@ void stage_cut_tree(const abfs_tree *tr, const double *static24, uint64_t n,
 
 // Plain cooperative launch of the default megakernel variant (partitions).
 int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device) {
-    static int grid = 0;
+    // co-resident grid per device (processes may drive GPUs of different
+    // occupancy); written once per device, same value from any thread
+    static int grids[64] = {0};
+    if (device < 0 || device >= 64) return fail(ABFS_EINVAL, "device ordinal out of range");
+    int &grid = grids[device];
     void *kfn = (void *)k_mega<5>;
     if (!grid) {
         int per = 0, sms = 0;
@@ -580,7 +608,7 @@ int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device) {
 
 static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, bool host_init,
                     int fixed_pair, const abfs_tree *tr, const double *static24, int64_t chunk,
-                    size_t *n_levels) {
+                    size_t *n_levels, uint64_t *checksums = nullptr) {
     const DevGraph &g = t->g->d;
     cudaStream_t s = t->stream;
     ABFS_CUDA(cudaSetDevice(t->device));
@@ -594,6 +622,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaHostGetDevicePointer((void **)&t->dnlev, t->mnlev, 0));
         ABFS_CUDA(cudaMallocHost((void **)&t->hroots, kMaxBatch * sizeof(uint32_t)));
         ABFS_CUDA(cudaMalloc((void **)&t->droots, kMaxBatch * sizeof(uint32_t)));
+        ABFS_CUDA(cudaMalloc((void **)&t->dsums, kMaxBatch * sizeof(unsigned long long)));
     }
     if (nroots < 1 || nroots > kMaxBatch) return fail(ABFS_EINVAL, "bad root count");
     void *kfn = t->mega_minb == 4   ? (void *)k_mega<4>
@@ -717,7 +746,13 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.xcount = nullptr;
     P.gcount = nullptr;
     P.xseq0 = 0;
+    P.checksums = nullptr;
+    if (checksums) {
+        ABFS_CUDA(cudaMemsetAsync(t->dsums, 0, nroots * sizeof(unsigned long long), s));
+        P.checksums = t->dsums;
+    }
     for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
+    std::lock_guard<std::mutex> mega_guard(g_mega_mu[t->device & 63]);
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
     if (t->mega_cluster) {
@@ -752,6 +787,9 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     t->launches += 1;
     ABFS_CUDA(cudaEventRecord(t->ev[1], s));
     ABFS_CUDA(cudaStreamSynchronize(s));
+    if (checksums)
+        ABFS_CUDA(cudaMemcpy(checksums, t->dsums, nroots * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost));
     unsigned long long tot = 0;
     for (size_t i = 0; i < nroots; ++i) tot += ((volatile unsigned long long *)t->mnlev)[i];
     const unsigned long long nl = ((volatile unsigned long long *)t->mnlev)[nroots - 1];
@@ -791,6 +829,7 @@ static uint64_t rec_ns(const MegaRecord &r) {
 
 extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_LOCK(t);
     t->use_mega = device_loop != 0;
     const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 6 : 5;
     if (minb != t->mega_minb) {
@@ -804,6 +843,7 @@ extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int va
                              int64_t chunk, int32_t *depths_out, uint64_t *counts,
                              uint64_t *elapsed, size_t cap, size_t *n_levels) {
     if (!t || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_TRY(level_params_ok(0, kernel, variant, chunk));
     if (t->use_mega) {
         if (root < 0 || (uint64_t)root >= t->g->d.n)
@@ -812,13 +852,18 @@ extern "C" int abfs_bfs_full(abfs_traversal *t, int64_t root, int kernel, int va
         size_t nl = 0;
         const uint32_t r32 = (uint32_t)root;
         ABFS_TRY(mega_run(t, &r32, 1, true, kernel * 3 + variant, nullptr, nullptr, chunk, &nl));
-        *n_levels = nl;
-        for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
-            if (counts) counts[l] = t->hrecs[l].new_count;
-            if (elapsed) elapsed[l] = rec_ns(t->hrecs[l]);
+        // more levels than the megakernel keeps records for (> kMegaCap): the
+        // launch-path driver below reports every level (the reference returns
+        // them all, kernels.py:356-371)
+        if (!((counts || elapsed) && nl > t->hrecs.size() && cap > t->hrecs.size())) {
+            *n_levels = nl;
+            for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
+                if (counts) counts[l] = t->hrecs[l].new_count;
+                if (elapsed) elapsed[l] = rec_ns(t->hrecs[l]);
+            }
+            if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
+            return ABFS_OK;
         }
-        if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
-        return ABFS_OK;
     }
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
@@ -906,6 +951,7 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
                                  const double *static24, int64_t chunk, int32_t *depths_out,
                                  abfs_level_record *recs, size_t cap, size_t *n_levels) {
     if (!t || !static24 || !n_levels) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_TRY(tree_ok(tr));
     if (t->use_mega) {
         if (root < 0 || (uint64_t)root >= t->g->d.n)
@@ -914,6 +960,8 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
         size_t nl = 0;
         const uint32_t r32 = (uint32_t)root;
         ABFS_TRY(mega_run(t, &r32, 1, true, -1, tr, static24, chunk, &nl));
+        if (recs && nl > t->hrecs.size() && cap > t->hrecs.size())
+            goto launch_path;   // > kMegaCap levels: the launch path records them all
         *n_levels = nl;
         if (recs)
             for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
@@ -933,6 +981,7 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
         if (depths_out) ABFS_TRY(abfs_read_depths(t, depths_out));
         return ABFS_OK;
     }
+launch_path:
     ABFS_TRY(init_impl(t, root));
     ABFS_CUDA(cudaEventRecord(t->et0, t->stream));
     uint64_t frontier = 1, discovered = 1;
@@ -978,18 +1027,21 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
 
 extern "C" int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches) {
     if (!t || !launches) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     *launches = t->launches;
     return ABFS_OK;
 }
 
 extern "C" int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns) {
     if (!t || !ns) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     *ns = t->last_trav_ns;
     return ABFS_OK;
 }
 
 extern "C" int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *vertices) {
     if (!t || !edges || !vertices) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_CUDA(cudaSetDevice(t->device));
     ABFS_CUDA(cudaMemsetAsync(&t->dctr->reached_edges, 0, 16, t->stream));
     k_reached<<<148 * 8, kBlock, 0, t->stream>>>(t->depth, t->g->d.out_off, t->g->d.n, t->dctr);
@@ -1032,6 +1084,7 @@ extern "C" int abfs_aggregate_count(int device, const int64_t *host_counts, size
 
 extern "C" int abfs_traversal_instrument(abfs_traversal *t, int on) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_LOCK(t);
     t->instrument = on != 0;
     t->es_log.clear();
     return ABFS_OK;
@@ -1040,6 +1093,7 @@ extern "C" int abfs_traversal_instrument(abfs_traversal *t, int on) {
 extern "C" int abfs_traversal_level_stats(abfs_traversal *t, size_t nlev, uint64_t *count,
                                           uint64_t *out_deg, uint64_t *in_deg, uint64_t *scanned) {
     if (!t || !count || !out_deg || !in_deg) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     ABFS_CUDA(cudaSetDevice(t->device));
     unsigned long long *h = nullptr;
     const size_t cells = 3 * (nlev + 1);
@@ -1077,11 +1131,13 @@ extern "C" int abfs_host_unregister(void *ptr) {
     return ABFS_OK;
 }
 
-extern "C" int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, size_t nroots,
-                                       const abfs_tree *tr, const double *static24,
-                                       int64_t chunk, uint64_t *levels, uint64_t *bfs_ns,
-                                       uint64_t *total_ns) {
+static int batch_impl(abfs_traversal *t, const int64_t *roots, size_t nroots,
+                      const abfs_tree *tr, const double *static24, int64_t chunk,
+                      uint64_t *levels, uint64_t *bfs_ns, uint64_t *total_ns,
+                      uint64_t *checksums, uint64_t *new_counts, size_t counts_cap,
+                      size_t *n_counts) {
     if (!t || !roots || !static24) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
     if (nroots < 1 || nroots > kMaxBatch)
         return fail(ABFS_EINVAL, "need 1.." + std::to_string(kMaxBatch) + " roots per batch");
     ABFS_TRY(tree_ok(tr));
@@ -1094,7 +1150,7 @@ extern "C" int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, 
         r32[i] = (uint32_t)roots[i];
     }
     size_t nl = 0;
-    ABFS_TRY(mega_run(t, r32.data(), nroots, false, -1, tr, static24, chunk, &nl));
+    ABFS_TRY(mega_run(t, r32.data(), nroots, false, -1, tr, static24, chunk, &nl, checksums));
     if (total_ns) *total_ns = t->last_trav_ns;
     size_t off = 0;
     for (size_t i = 0; i < nroots; ++i) {
@@ -1111,5 +1167,34 @@ extern "C" int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, 
         }
         off += li;
     }
+    if (n_counts) {
+        // every root's per-level new counts, concatenated (records kept: the
+        // first kMegaCap levels of the launch)
+        const size_t k = std::min(t->batch_recs, counts_cap);
+        for (size_t l = 0; new_counts && l < k; ++l) new_counts[l] = t->mrecs[l].new_count;
+        *n_counts = t->batch_recs;
+    }
     return ABFS_OK;
+}
+
+extern "C" int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, size_t nroots,
+                                       const abfs_tree *tr, const double *static24,
+                                       int64_t chunk, uint64_t *levels, uint64_t *bfs_ns,
+                                       uint64_t *total_ns) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    ABFS_LOCK(t);
+    return batch_impl(t, roots, nroots, tr, static24, chunk, levels, bfs_ns, total_ns, nullptr,
+                      nullptr, 0, nullptr);
+}
+
+extern "C" int abfs_adaptive_bfs_batch_check(abfs_traversal *t, const int64_t *roots,
+                                             size_t nroots, const abfs_tree *tr,
+                                             const double *static24, int64_t chunk,
+                                             uint64_t *levels, uint64_t *checksums,
+                                             uint64_t *new_counts, size_t counts_cap,
+                                             size_t *n_counts) {
+    if (!t || !checksums) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
+    return batch_impl(t, roots, nroots, tr, static24, chunk, levels, nullptr, nullptr, checksums,
+                      new_counts, counts_cap, n_counts);
 }

@@ -20,6 +20,10 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
 #include "common.cuh"
 
 using namespace abfs;
@@ -507,4 +511,140 @@ extern "C" int abfs_graph_generate_mesh(int device, uint32_t rows, uint32_t cols
     cudaFree(cur);
     *out = g;
     return finish_build(rc, g, out);
+}
+
+// ---- ADGR files on the engine side ---------------------------
+
+namespace {
+
+// Python's repr() of a bytes object (the reference's error texts quote the
+// magic with {magic!r}).
+std::string bytes_repr(const unsigned char *b, size_t n) {
+    bool sq = false, dq = false;
+    for (size_t i = 0; i < n; ++i) {
+        sq |= b[i] == '\'';
+        dq |= b[i] == '"';
+    }
+    const char q = (sq && !dq) ? '"' : '\'';
+    std::string s = "b";
+    s += q;
+    static const char *hex = "0123456789abcdef";
+    for (size_t i = 0; i < n; ++i) {
+        const unsigned char c = b[i];
+        if (c == (unsigned char)q || c == '\\') {
+            s += '\\';
+            s += (char)c;
+        } else if (c == '\t') {
+            s += "\\t";
+        } else if (c == '\n') {
+            s += "\\n";
+        } else if (c == '\r') {
+            s += "\\r";
+        } else if (c < 0x20 || c >= 0x7f) {
+            s += "\\x";
+            s += hex[c >> 4];
+            s += hex[c & 15];
+        } else {
+            s += (char)c;
+        }
+    }
+    s += q;
+    return s;
+}
+
+struct File {
+    FILE *f = nullptr;
+    ~File() {
+        if (f) fclose(f);
+    }
+};
+
+}  // namespace
+
+extern "C" int abfs_graph_read(int device, const char *path, abfs_graph **out) {
+    // read_graph (graph.py:304-324): "ADGR", <IQQ> (version 1, |V|, |E|),
+    // five little-endian u32 arrays; the arrays are streamed through a pinned
+    // buffer straight into HBM (no host copy of the graph).
+    if (!path || !out) return fail(ABFS_EINVAL, "null argument");
+    File fh;
+    fh.f = fopen(path, "rb");
+    if (!fh.f) return fail(ABFS_EINVAL, std::string("cannot open graph file ") + path);
+    unsigned char magic[4];
+    const size_t got = fread(magic, 1, 4, fh.f);
+    if (got != 4 || std::memcmp(magic, "ADGR", 4) != 0)
+        return fail(ABFS_EINVAL, "bad magic " + bytes_repr(magic, got) + " in graph file " + path);
+    unsigned char hdr[20];
+    if (fread(hdr, 1, 20, fh.f) != 20) return fail(ABFS_EINVAL, std::string("truncated graph header in ") + path);
+    uint32_t version;
+    uint64_t n, m;
+    std::memcpy(&version, hdr, 4);
+    std::memcpy(&n, hdr + 4, 8);
+    std::memcpy(&m, hdr + 12, 8);
+    if (version != 1) return fail(ABFS_EINVAL, "unsupported graph format version " + std::to_string(version));
+    abfs_graph *g = nullptr;
+    ABFS_TRY(new_graph(device, n, m, &g));
+    DevGraph &d = g->d;
+    const size_t chunk = 16u << 20;
+    char *stage = nullptr;
+    int rc = ABFS_OK;
+    if (cudaMallocHost(&stage, chunk) != cudaSuccess) rc = fail(ABFS_ENOMEM, "pinned staging buffer");
+    uint32_t *dst_of[5] = {d.out_off, d.dst, d.org, d.in_off, d.src};
+    const uint64_t cnt_of[5] = {n + 1, m, m, n + 1, m};
+    for (int a = 0; a < 5 && rc == ABFS_OK; ++a) {
+        const uint64_t bytes = cnt_of[a] * 4;
+        for (uint64_t off = 0; off < bytes && rc == ABFS_OK; off += chunk) {
+            const size_t len = (size_t)std::min<uint64_t>(chunk, bytes - off);
+            if (fread(stage, 1, len, fh.f) != len) {
+                rc = fail(ABFS_EINVAL, std::string("truncated graph file ") + path);
+                break;
+            }
+            const cudaError_t e = cudaMemcpy(reinterpret_cast<char *>(dst_of[a]) + off, stage, len,
+                                             cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("graph_read: ") + cudaGetErrorString(e));
+        }
+    }
+    if (rc == ABFS_OK && fgetc(fh.f) != EOF) rc = fail(ABFS_EINVAL, std::string("trailing bytes in graph file ") + path);
+    if (stage) cudaFreeHost(stage);
+    if (rc == ABFS_OK && m) {
+        k_rev_owner<<<grid_cap(m, 256), 256>>>(d.in_off, n, m, d.rev_owner);
+        const cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("rev_owner: ") + cudaGetErrorString(e));
+    }
+    *out = g;
+    return finish_build(rc, g, out);
+}
+
+extern "C" int abfs_graph_write(const abfs_graph *g, const char *path) {
+    // write_graph (graph.py:292-301): same bytes as the reference writer.
+    if (!g || !path) return fail(ABFS_EINVAL, "null argument");
+    ABFS_CUDA(cudaSetDevice(g->device));
+    File fh;
+    fh.f = fopen(path, "wb");
+    if (!fh.f) return fail(ABFS_EINVAL, std::string("cannot create graph file ") + path);
+    const DevGraph &d = g->d;
+    unsigned char hdr[24];
+    const uint32_t version = 1;
+    std::memcpy(hdr, "ADGR", 4);
+    std::memcpy(hdr + 4, &version, 4);
+    std::memcpy(hdr + 8, &d.n, 8);
+    std::memcpy(hdr + 16, &d.m, 8);
+    if (fwrite(hdr, 1, 24, fh.f) != 24) return fail(ABFS_EINVAL, std::string("write failed: ") + path);
+    const size_t chunk = 16u << 20;
+    char *stage = nullptr;
+    ABFS_CUDA(cudaMallocHost(&stage, chunk));
+    const uint32_t *src_of[5] = {d.out_off, d.dst, d.org, d.in_off, d.src};
+    const uint64_t cnt_of[5] = {d.n + 1, d.m, d.m, d.n + 1, d.m};
+    int rc = ABFS_OK;
+    for (int a = 0; a < 5 && rc == ABFS_OK; ++a) {
+        const uint64_t bytes = cnt_of[a] * 4;
+        for (uint64_t off = 0; off < bytes && rc == ABFS_OK; off += chunk) {
+            const size_t len = (size_t)std::min<uint64_t>(chunk, bytes - off);
+            const cudaError_t e = cudaMemcpy(stage, reinterpret_cast<const char *>(src_of[a]) + off, len,
+                                             cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) rc = fail(ABFS_ECUDA, std::string("graph_write: ") + cudaGetErrorString(e));
+            else if (fwrite(stage, 1, len, fh.f) != len) rc = fail(ABFS_EINVAL, std::string("write failed: ") + path);
+        }
+    }
+    cudaFreeHost(stage);
+    return rc;
 }

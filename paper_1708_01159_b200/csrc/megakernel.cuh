@@ -15,6 +15,7 @@
 
 #include <cooperative_groups.h>
 
+#include <mutex>
 #include <vector>
 
 #include "bfs_kernels.cuh"
@@ -81,7 +82,17 @@ struct MegaParams {
     unsigned long long *xcount; // slice popc accumulator
     unsigned long long *gcount; // global level count of the last exchange
     unsigned long long xseq0;   // exchanges completed before this launch
+    // optional [nroots]: per-root depth checksum (depth_mix) of the final
+    // depth array of each traversal, for batch parity checks
+    unsigned long long *checksums;
 };
+
+// Order-sensitive checksum term of one vertex's depth (numpy restatement in
+// tests: sum over v of (uint64(uint32(d)) + 1) * ((v + 1) * 0x9E3779B97F4A7C15),
+// all mod 2^64).
+__device__ __forceinline__ unsigned long long depth_mix(uint64_t v, int32_t d) {
+    return ((unsigned long long)(uint32_t)d + 1ull) * ((v + 1ull) * 0x9E3779B97F4A7C15ull);
+}
 
 // Hand-off from cluster 0 back to the grid after a solo run.
 struct SoloState {
@@ -95,6 +106,7 @@ struct SoloState {
 void stage_cut_tree(const abfs_tree *tr, const double *static24, uint64_t n,
                     std::vector<unsigned char> &blob, uint32_t &nn);
 int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device);
+std::mutex &mega_mutex(int device);   // held from a megakernel launch to its completion
 
 constexpr uint32_t kMegaCapPart = 1u << 16;   // level records of a partition's loop
 constexpr uint32_t kSoloUnits = 16;   // more CTA units than this: hand the level to the grid
@@ -608,6 +620,17 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         cur ^= 1;
         has_q = P.part ? false : topdown;   // a partition's next frontier is the gathered bitmap
         has_bm = P.part ? true : !topdown;
+    }
+    if (P.checksums) {
+        // the traversal's last level ended at a grid barrier: every depth is final
+        const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+        const uint64_t nt = (uint64_t)gridDim.x * kBlock;
+        unsigned long long acc = 0;
+        for (uint64_t v = P.lo + tid; v < P.hi; v += nt) acc += depth_mix(v, P.depth[v]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(P.checksums + ri, acc);
+        grid.sync();   // before the next root's init overwrites the depths
     }
     }   // roots
 }

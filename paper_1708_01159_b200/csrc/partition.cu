@@ -26,6 +26,7 @@
 
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "launch.cuh"
@@ -35,6 +36,7 @@ using namespace abfs;
 
 
 struct abfs_part {
+    mutable std::recursive_mutex mu;   // per-handle lock
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -425,6 +427,7 @@ extern "C" int abfs_part_info(const abfs_part *p, uint64_t *lo, uint64_t *hi, ui
 
 extern "C" int abfs_part_set_stream(abfs_part *p, void *stream) {
     if (!p) return fail(ABFS_EINVAL, "null partition");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     ABFS_CUDA(cudaSetDevice(p->device));
     ABFS_CUDA(cudaStreamSynchronize(p->stream));
     if (p->own_stream) cudaStreamDestroy(p->stream);
@@ -437,6 +440,7 @@ extern "C" int abfs_part_set_stream(abfs_part *p, void *stream) {
 
 extern "C" int abfs_part_init(abfs_part *p, int64_t root) {
     if (!p) return fail(ABFS_EINVAL, "null partition");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (root < 0 || (uint64_t)root >= p->n)
         return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
                                      std::to_string(p->n));
@@ -517,6 +521,7 @@ static int part_strategy(abfs_part *p, int64_t level, int kernel, int variant, i
 extern "C" int abfs_part_level(abfs_part *p, int64_t level, int kernel, int variant,
                                int64_t chunk, uint32_t *send, uint64_t stride) {
     if (!p || !send) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (stride < p->nwl) return fail(ABFS_EINVAL, "send stride smaller than the owned slice");
     ABFS_TRY(part_strategy(p, level, kernel, variant, chunk));
     k_part_pack<<<grid_for(stride, kBlock, 148 * 16), kBlock, 0, p->stream>>>(
@@ -530,6 +535,7 @@ extern "C" int abfs_part_exchange(abfs_part *p, const uint32_t *gathered, const 
                                   uint32_t nranks, uint64_t stride, uint64_t *global_count,
                                   uint64_t *local_count, uint64_t *elapsed_ns) {
     if (!p || !gathered || !word_bounds || !global_count) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (p->last_kernel < 0) return fail(ABFS_EINVAL, "exchange without a level");
     if (nranks < 1 || nranks > kMaxRanks) return fail(ABFS_EINVAL, "bad rank count");
     Bounds b;
@@ -573,6 +579,7 @@ extern "C" int abfs_part_exchange(abfs_part *p, const uint32_t *gathered, const 
 
 extern "C" int abfs_part_read_depths(abfs_part *p, int32_t *host_owned) {
     if (!p || !host_owned) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     ABFS_CUDA(cudaSetDevice(p->device));
     ABFS_CUDA(cudaMemcpyAsync(host_owned, p->depth, p->nv * 4, cudaMemcpyDeviceToHost, p->stream));
     ABFS_CUDA(cudaStreamSynchronize(p->stream));
@@ -581,6 +588,7 @@ extern "C" int abfs_part_read_depths(abfs_part *p, int32_t *host_owned) {
 
 extern "C" int abfs_part_depths_device(abfs_part *p, int32_t *dev_out) {
     if (!p || !dev_out) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     ABFS_CUDA(cudaSetDevice(p->device));
     ABFS_CUDA(cudaMemcpyAsync(dev_out, p->depth, p->nv * 4, cudaMemcpyDeviceToDevice, p->stream));
     return ABFS_OK;
@@ -627,6 +635,7 @@ extern "C" int abfs_part_peer_buffers(abfs_part *p, void **fbm0, void **fbm1, vo
 extern "C" int abfs_part_set_peers(abfs_part *p, void *const *fbm0, void *const *fbm1,
                                    void *const *mailboxes, uint32_t nranks, uint32_t rank) {
     if (!p || !fbm0 || !fbm1 || !mailboxes) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (nranks < 1 || nranks > kMaxRanks || rank >= nranks) return fail(ABFS_EINVAL, "bad rank count");
     if (fbm0[rank] != p->fbm[0] || fbm1[rank] != p->fbm[1] || mailboxes[rank] != p->box)
         return fail(ABFS_EINVAL, "own buffers must sit at this rank's slot");
@@ -654,6 +663,7 @@ extern "C" int abfs_part_ipc_export(abfs_part *p, unsigned char *handles) {
 extern "C" int abfs_part_ipc_open(abfs_part *p, const unsigned char *all_handles, uint32_t nranks,
                                   uint32_t rank) {
     if (!p || !all_handles) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (nranks < 1 || nranks > kMaxRanks || rank >= nranks) return fail(ABFS_EINVAL, "bad rank count");
     ABFS_CUDA(cudaSetDevice(p->device));
     std::vector<uint32_t *> f0(nranks), f1(nranks);
@@ -682,6 +692,7 @@ extern "C" int abfs_part_ipc_open(abfs_part *p, const unsigned char *all_handles
 extern "C" int abfs_part_level_p2p(abfs_part *p, int64_t level, int kernel, int variant,
                                    int64_t chunk) {
     if (!p) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (!p->nranks) return fail(ABFS_EINVAL, "peers not set (abfs_part_set_peers / abfs_part_ipc_open)");
     ABFS_TRY(part_strategy(p, level, kernel, variant, chunk));
     const int parity = (int)(p->p2p_seq & 1);
@@ -697,6 +708,7 @@ extern "C" int abfs_part_level_p2p(abfs_part *p, int64_t level, int kernel, int 
 extern "C" int abfs_part_p2p_finish(abfs_part *p, uint64_t *global_count, uint64_t *local_count,
                                     uint64_t *elapsed_ns) {
     if (!p || !global_count) return fail(ABFS_EINVAL, "null argument");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (p->last_kernel < 0) return fail(ABFS_EINVAL, "finish without a level");
     ABFS_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = p->stream;
@@ -821,6 +833,7 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
                      uint64_t *local_counts, size_t cap, size_t *n_levels) {
     if (!p || !n_levels) return fail(ABFS_EINVAL, "null argument");
     if (!p->nranks) return fail(ABFS_EINVAL, "peers not set (abfs_part_set_peers / abfs_part_ipc_open)");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
     if (root < 0 || (uint64_t)root >= p->n)
         return fail(ABFS_EINVAL, "root " + std::to_string(root) + " out of range for |V|=" +
                                      std::to_string(p->n));
@@ -902,11 +915,14 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     P.gcount = p->dx + 1;
     P.xseq0 = p->p2p_seq;
     *(volatile unsigned long long *)p->mnlev = 0;
-    ABFS_CUDA(cudaEventRecord(p->e0, s));
-    ABFS_TRY(mega_launch_plain(P, s, p->device));
-    p->launches += 1;
-    ABFS_CUDA(cudaEventRecord(p->e1, s));
-    ABFS_CUDA(cudaStreamSynchronize(s));
+    {
+        std::lock_guard<std::mutex> mega_guard(mega_mutex(p->device));
+        ABFS_CUDA(cudaEventRecord(p->e0, s));
+        ABFS_TRY(mega_launch_plain(P, s, p->device));
+        p->launches += 1;
+        ABFS_CUDA(cudaEventRecord(p->e1, s));
+        ABFS_CUDA(cudaStreamSynchronize(s));
+    }
     const unsigned long long nl = *(volatile unsigned long long *)p->mnlev;
     p->p2p_seq += nl;
     p->last_kernel = -1;
@@ -915,6 +931,14 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     ABFS_CUDA(cudaMemcpy(&timed_out, &p->box->timeout, sizeof(int), cudaMemcpyDeviceToHost));
     if (timed_out) return fail(ABFS_ENCCL, "peer exchange timed out (a rank never signalled a level)");
     const size_t keep = nl < kMegaCapPart ? (size_t)nl : kMegaCapPart;
+    if ((recs || local_counts) && nl > keep && cap > keep) {
+        // more levels than the persistent loop keeps records for: redo the
+        // traversal with the host-driven fused-exchange loop, which records
+        // every level (nl is global, so every rank takes this branch)
+        abfs_part *const one[1] = {p};
+        return parts_traverse(one, 1, root, tr, static24, fixed_pair, chunk, recs, local_counts,
+                              cap, n_levels);
+    }
     for (size_t l = 0; recs && l < keep && l < cap; ++l) {
         const MegaRecord &m = p->mrecs[l];
         abfs_level_record &r = recs[l];

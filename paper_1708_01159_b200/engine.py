@@ -8,7 +8,9 @@ objects the reference-named functions in kernels.py / adaptive.py drive.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import threading
 
 import numpy as np
 
@@ -18,7 +20,7 @@ from . import _lib as L
 class DeviceGraph:
     """A Graph (graph.py:27-69) resident on one GPU."""
 
-    def __init__(self, handle: ctypes.c_void_p, host=None):
+    def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
         n, m, dev = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int()
         L.check(L.lib().abfs_graph_info(handle, ctypes.byref(n), ctypes.byref(m),
@@ -26,8 +28,14 @@ class DeviceGraph:
         self.vertex_count = n.value
         self.edge_count = m.value
         self.device = dev.value
-        self._host = host
         self._scratch = None
+        # traversal pool of the stateless reference-style calls: the primary
+        # (`scratch()`) serves single-threaded use; concurrent callers on the
+        # same graph get their own Traversal (distinct
+        # traversals of one immutable Graph may run concurrently)
+        self._pool_lock = threading.Lock()
+        self._idle: list = []
+        self._primary_busy = False
 
     # -- constructors -------------------------------------------------------
     @classmethod
@@ -38,7 +46,7 @@ class DeviceGraph:
         L.check(L.lib().abfs_graph_upload(device, graph.vertex_count, graph.edge_count,
                                           *[L.ptr(x, L.u32p) for x in a], ctypes.byref(h)),
                 "graph_upload")
-        return cls(h, host=graph)
+        return cls(h)
 
     @classmethod
     def build(cls, vertex_count: int, src, dst, device: int = 0) -> "DeviceGraph":
@@ -111,12 +119,44 @@ class DeviceGraph:
                      a["origins"], a["in_offsets"], a["sources"])
 
     def scratch(self) -> "Traversal":
-        """Cached traversal used by the stateless reference-style calls."""
-        if self._scratch is None:
-            self._scratch = Traversal(self)
-        return self._scratch
+        """The primary traversal of the stateless reference-style calls
+        (its level-loop mode is inherited by the pool's other traversals)."""
+        with self._pool_lock:
+            if self._scratch is None:
+                self._scratch = Traversal(self)
+            return self._scratch
+
+    @contextlib.contextmanager
+    def borrow(self):
+        """A traversal no other thread is using, for one reference-style call
+        (the primary when it is free, else a pooled or new one)."""
+        with self._pool_lock:
+            if self._scratch is None:
+                self._scratch = Traversal(self)
+            t = None
+            if not self._primary_busy:
+                self._primary_busy = True
+                t = self._scratch
+            elif self._idle:
+                t = self._idle.pop()
+            mode = self._scratch.mode
+        if t is None:
+            t = Traversal(self)
+        if t is not self._scratch and t.mode != mode:
+            t.set_device_loop(mode)
+        try:
+            yield t
+        finally:
+            with self._pool_lock:
+                if t is self._scratch:
+                    self._primary_busy = False
+                else:
+                    self._idle.append(t)
 
     def close(self):
+        for t in self._idle:
+            t.close()
+        self._idle = []
         if self._scratch is not None:
             self._scratch.close()
             self._scratch = None
@@ -136,6 +176,7 @@ class Traversal:
 
     def __init__(self, dgraph: DeviceGraph):
         self.graph = dgraph
+        self.mode = 1
         self._h = ctypes.c_void_p()
         L.check(L.lib().abfs_traversal_create(dgraph._h, ctypes.byref(self._h)),
                 "traversal_create")
@@ -174,27 +215,35 @@ class Traversal:
         return c.value, el.value
 
     def bfs_full(self, root: int, kernel: int, variant: int, chunk_size: int = 32,
-                 depths_out: np.ndarray | None = None, cap: int = 1 << 20):
-        counts, el = self._level_arrays(cap)
-        nl = ctypes.c_size_t()
-        L.check(L.lib().abfs_bfs_full(self._h, int(root), int(kernel), int(variant),
-                                      int(chunk_size),
-                                      L.ptr(depths_out, L.i32p) if depths_out is not None else None,
-                                      L.ptr(counts, L.u64p), L.ptr(el, L.u64p), cap,
-                                      ctypes.byref(nl)), "bfs_full")
-        k = min(nl.value, cap)
-        return counts[:k].copy(), el[:k].copy()
+                 depths_out: np.ndarray | None = None, cap: int = 1 << 16):
+        """Every level's (count, ns); a traversal with more than `cap` levels
+        is re-run with room for all of them (the reference returns every
+        level, kernels.py:356-371)."""
+        while True:
+            counts, el = self._level_arrays(cap)
+            nl = ctypes.c_size_t()
+            L.check(L.lib().abfs_bfs_full(self._h, int(root), int(kernel), int(variant),
+                                          int(chunk_size),
+                                          L.ptr(depths_out, L.i32p) if depths_out is not None else None,
+                                          L.ptr(counts, L.u64p), L.ptr(el, L.u64p), cap,
+                                          ctypes.byref(nl)), "bfs_full")
+            if nl.value <= cap:
+                return counts[:nl.value].copy(), el[:nl.value].copy()
+            cap = nl.value
 
     def adaptive(self, root: int, tree: L.AbfsTree, static24: np.ndarray, chunk_size: int = 32,
                  depths_out: np.ndarray | None = None, cap: int = 1 << 16):
-        recs = self._records(cap)
-        nl = ctypes.c_size_t()
         st = np.ascontiguousarray(static24, dtype=np.float64)
-        L.check(L.lib().abfs_adaptive_bfs(
-            self._h, int(root), ctypes.byref(tree), L.ptr(st, L.f64p), int(chunk_size),
-            L.ptr(depths_out, L.i32p) if depths_out is not None else None, recs, cap,
-            ctypes.byref(nl)), "adaptive_bfs")
-        return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:min(nl.value, cap)]]
+        while True:
+            recs = self._records(cap)
+            nl = ctypes.c_size_t()
+            L.check(L.lib().abfs_adaptive_bfs(
+                self._h, int(root), ctypes.byref(tree), L.ptr(st, L.f64p), int(chunk_size),
+                L.ptr(depths_out, L.i32p) if depths_out is not None else None, recs, cap,
+                ctypes.byref(nl)), "adaptive_bfs")
+            if nl.value <= cap:
+                return [L.AbfsLevelRecord.from_buffer_copy(r) for r in recs[:nl.value]]
+            cap = nl.value   # more levels than records: re-run with room for all
 
     def adaptive_batch(self, roots, tree: L.AbfsTree, static24: np.ndarray,
                        chunk_size: int = 32):
@@ -210,6 +259,27 @@ class Traversal:
                                                 L.ptr(ns, L.u64p), ctypes.byref(tot)),
                 "adaptive_bfs_batch")
         return lv, ns, tot.value
+
+    def adaptive_batch_check(self, roots, tree: L.AbfsTree, static24: np.ndarray,
+                             chunk_size: int = 32):
+        """The batch with per-root parity evidence: (levels, depth checksums,
+        per-root lists of per-level new counts).  See depth_checksum()."""
+        r = np.ascontiguousarray(roots, dtype=np.int64)
+        lv = np.zeros(r.size, np.uint64)
+        cs = np.zeros(r.size, np.uint64)
+        cap = 1 << 16
+        nc = np.zeros(cap, np.uint64)
+        n = ctypes.c_size_t()
+        st = np.ascontiguousarray(static24, dtype=np.float64)
+        L.check(L.lib().abfs_adaptive_bfs_batch_check(
+            self._h, L.ptr(r, L.i64p), r.size, ctypes.byref(tree), L.ptr(st, L.f64p),
+            int(chunk_size), L.ptr(lv, L.u64p), L.ptr(cs, L.u64p), L.ptr(nc, L.u64p), cap,
+            ctypes.byref(n)), "adaptive_bfs_batch_check")
+        per, off = [], 0
+        for k in lv.tolist():
+            per.append(nc[off:off + k].tolist() if off + k <= min(n.value, cap) else None)
+            off += k
+        return lv, cs, per
 
     def _records(self, cap: int):
         # one record buffer per traversal (allocating 3.6 MB per call would
@@ -236,6 +306,7 @@ class Traversal:
         """True/1 (default): whole traversals run in the persistent megakernel
         (2: its 64-register variant); False/0: per-level launches."""
         L.check(L.lib().abfs_traversal_set_mode(self._h, int(on)), "set_mode")
+        self.mode = int(on)
 
     def launches(self) -> int:
         v = ctypes.c_uint64()
@@ -277,3 +348,13 @@ def pcg_words(seed: int):
     s, i = st["state"], st["inc"]
     return (np.array([s >> 64, s & m64], dtype=np.uint64),
             np.array([i >> 64, i & m64], dtype=np.uint64))
+
+
+def depth_checksum(depths: np.ndarray) -> int:
+    """Host restatement of the batch kernel's per-root depth checksum:
+    sum over v of (uint64(uint32(d[v])) + 1) * ((v + 1) * 0x9E3779B97F4A7C15)
+    mod 2^64 (abfs_adaptive_bfs_batch_check)."""
+    d = np.asarray(depths).astype(np.int64).astype(np.uint32).astype(np.uint64) + np.uint64(1)
+    w = (np.arange(1, d.size + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15))
+    with np.errstate(over="ignore"):
+        return int((d * w).sum(dtype=np.uint64))

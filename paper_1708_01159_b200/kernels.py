@@ -21,6 +21,7 @@ HBM for the whole traversal and copies the depths back once.
 from __future__ import annotations
 
 import ctypes
+import threading
 from collections import deque
 from dataclasses import dataclass
 from enum import IntEnum
@@ -88,28 +89,45 @@ def worker_count() -> int:
 
 
 _foreign_uploads: dict = {}
+_foreign_lock = threading.Lock()
 
 
 def _device(graph):
     """DeviceGraph for a host Graph (cached upload), a DeviceGraph, or any
-    object with the reference Graph's fields (e.g. an adaptive_bfs.Graph),
-    uploaded once and cached for the object's lifetime."""
+    object with the reference Graph's fields (e.g. an adaptive_bfs.Graph).
+
+    A foreign graph's upload is cached under id(graph) together with a weak
+    reference to it, and evicted when the graph is collected; every hit is
+    checked against the weak reference, so a recycled id never maps to
+    another graph's device copy.  Objects that cannot be weakly referenced
+    are uploaded per call (correct, uncached)."""
     if hasattr(graph, "device_graph"):
         return graph.device_graph()
     if hasattr(graph, "out_offsets") and hasattr(graph, "sources"):
+        import weakref
+        from .engine import DeviceGraph
         key = id(graph)
-        dg = _foreign_uploads.get(key)
-        if dg is None:
-            import weakref
-            from .engine import DeviceGraph
-            dg = DeviceGraph.upload(graph)
-            _foreign_uploads[key] = dg
-            try:
-                weakref.finalize(graph, _foreign_uploads.pop, key, None)
-            except TypeError:
-                pass
+        with _foreign_lock:
+            hit = _foreign_uploads.get(key)
+            if hit is not None and hit[0]() is graph:
+                return hit[1]
+        try:
+            ref = weakref.ref(graph)
+        except TypeError:
+            return DeviceGraph.upload(graph)
+        dg = DeviceGraph.upload(graph)
+        with _foreign_lock:
+            _foreign_uploads[key] = (ref, dg)
+        weakref.finalize(graph, _evict_foreign, key, ref)
         return dg
     return graph
+
+
+def _evict_foreign(key, ref) -> None:
+    with _foreign_lock:
+        hit = _foreign_uploads.get(key)
+        if hit is not None and hit[0] is ref:
+            del _foreign_uploads[key]
 
 
 def _check_root(graph, root: int) -> None:
@@ -121,9 +139,9 @@ def init_depths(graph, root: int) -> np.ndarray:
     """INF everywhere except depth 0 at root (kernels.py:134-140), built on
     the device and copied back."""
     _check_root(graph, root)
-    t = _device(graph).scratch()
-    t.init(root)
-    return t.read(depth_array(graph.vertex_count))
+    with _device(graph).borrow() as t:
+        t.init(root)
+        return t.read(depth_array(graph.vertex_count))
 
 
 def aggregate_count(local_counts, variant: CountVariant) -> int:
@@ -161,14 +179,14 @@ def run_level(graph, depths: np.ndarray, level: int, kernel: KernelId,
     (duck typing, e.g. int64) through an int32 staging copy.
     """
     k, v = _validate(kernel, variant, chunk_size)
-    t = _device(graph).scratch()
-    if (isinstance(depths, np.ndarray) and depths.dtype == np.int32
-            and depths.flags.c_contiguous and depths.flags.writeable):
-        c, el = t.run_level_host(depths, level, k, v, chunk_size)
-    else:
-        stage = np.ascontiguousarray(depths, dtype=np.int32)
-        c, el = t.run_level_host(stage, level, k, v, chunk_size)
-        depths[...] = stage
+    with _device(graph).borrow() as t:
+        if (isinstance(depths, np.ndarray) and depths.dtype == np.int32
+                and depths.flags.c_contiguous and depths.flags.writeable):
+            c, el = t.run_level_host(depths, level, k, v, chunk_size)
+        else:
+            stage = np.ascontiguousarray(depths, dtype=np.int32)
+            c, el = t.run_level_host(stage, level, k, v, chunk_size)
+            depths[...] = stage
     return LevelOutcome(new_frontier_count=int(c), elapsed_ns=int(el))
 
 
@@ -201,10 +219,9 @@ def bfs_full(graph, root: int, kernel: KernelId, variant: CountVariant,
     and recorded (kernels.py:356-371).  State stays in HBM throughout."""
     _check_root(graph, root)
     k, v = _validate(kernel, variant, chunk_size)
-    t = _device(graph).scratch()
     depths = depth_array(graph.vertex_count)
-    counts, elapsed = t.bfs_full(root, k, v, chunk_size, depths_out=depths,
-                                 cap=min(graph.vertex_count + 2, 1 << 20))
+    with _device(graph).borrow() as t:
+        counts, elapsed = t.bfs_full(root, k, v, chunk_size, depths_out=depths)
     return depths, [LevelOutcome(int(c), int(e)) for c, e in zip(counts, elapsed)]
 
 

@@ -1,0 +1,185 @@
+"""GPU parity on what the benchmark times and on config 1.
+
+* config 1 at full size (Kronecker 16, 64 roots) on the device-generated
+  graph: depth sha256, depth histogram and the (kernel, variant, fallback,
+  frontier) trace under the parity trees T1 and T4 equal the golden vectors
+  frozen from the unmodified reference (tests/golden/traces.json["k16"]),
+  through both level drivers;
+* the batched launch the bench times (abfs_adaptive_bfs_batch, in-kernel
+  init per root): every root's final depth array (in-kernel checksum) and
+  per-level counts equal the oracle's reference_bfs -- at K16 for all 64
+  roots and at K24 for the exact 8-root step bench.py times;
+* the GTEPS numerator (k_reached) and the work-model histogram
+  (k_level_hist, pull's scanned-edge counter) against host sums.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import golden_util as G
+import oracle
+import paper_1708_01159_b200 as P
+from paper_1708_01159_b200 import DeviceGraph, Traversal
+from paper_1708_01159_b200.engine import depth_checksum
+from paper_1708_01159_b200.features import static_vector
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INF = G.INF
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def trace_rows(tr):
+    return [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+            for x in tr.records]
+
+
+@pytest.fixture(scope="module")
+def k16():
+    meta = G.traces()["k16"]
+    dg = DeviceGraph.rmat(16, 16 << 16, 1, symmetrize=True)
+    yield dg, meta
+    dg.close()
+
+
+def test_config1_k16_64_roots_traces_both_drivers(k16):
+    dg, meta = k16
+    stats = P.compute_stats(dg)
+    st = static_vector(stats)
+    np.testing.assert_array_equal(st[6:], np.array(meta["stats"], np.float64))
+    t1 = P.deserialize(G.tree_path("t1"))
+    t4 = P.deserialize(G.tree_path("t4_k16"))
+    t = dg.scratch()
+    try:
+        for loop in (True, False):
+            t.set_device_loop(loop)
+            for r in meta["roots"]:
+                run = meta["runs"][str(r)]
+                for key, flat in (("t1", t1), ("t4", t4)):
+                    d, tr = P.adaptive_bfs(dg, r, flat, stats)
+                    assert sha(d) == run["depth_sha256"], (loop, r, key)
+                    assert trace_rows(tr) == run[key], (loop, r, key)
+                    assert np.bincount(d[d != INF]).tolist() == run["hist"]
+    finally:
+        t.set_device_loop(True)
+
+
+def test_config1_k16_fixed_pairs(k16):
+    dg, meta = k16
+    for i, r in enumerate(meta["roots"][:8]):
+        run = meta["runs"][str(r)]
+        for k, v in P.ALL_PAIRS[i % 3::3]:
+            d, outs = P.bfs_full(dg, r, k, v)
+            assert sha(d) == run["depth_sha256"], (r, k, v)
+            assert [o.new_frontier_count for o in outs] == run["hist"][1:] + [0]
+
+
+def _oracle_graph(dg):
+    a = dg.download(rev_owner=True)
+    return oracle.OracleGraph(dg.vertex_count, dg.edge_count, a["out_offsets"], a["destinations"],
+                              a["origins"], a["in_offsets"], a["sources"], a["rev_owner"])
+
+
+def _check_batch(dg, roots, model, og):
+    stats = P.compute_stats(dg)
+    t = Traversal(dg)
+    try:
+        lv, cs, per = t.adaptive_batch_check(roots, model.as_abfs(), static_vector(stats))
+        for i, r in enumerate(roots):
+            want = oracle.reference_bfs(og, r)
+            hist = np.bincount(want[want != INF]).tolist()
+            assert int(cs[i]) == depth_checksum(want), (i, r)
+            assert int(lv[i]) == len(hist), (i, r)
+            assert per[i] == hist[1:] + [0], (i, r)
+        # the checksum is order-sensitive: a swapped pair of depths changes it
+        d = oracle.reference_bfs(og, roots[-1])
+        j = np.flatnonzero(d != d[0])
+        if j.size:
+            e = d.copy()
+            e[0], e[j[0]] = d[j[0]], d[0]
+            assert depth_checksum(e) != depth_checksum(d)
+        np.testing.assert_array_equal(t.read(), oracle.reference_bfs(og, roots[-1]))
+    finally:
+        t.close()
+
+
+def test_config1_k16_batch_all_roots(k16):
+    dg, meta = k16
+    og = _oracle_graph(dg)
+    roots = list(meta["roots"])
+    _check_batch(dg, roots + roots[:5][::-1], P.deserialize(G.tree_path("t1")), og)
+    _check_batch(dg, roots[:16], P.deserialize(os.path.join(ROOT, "models", "gpu_tree.tree")), og)
+
+
+@pytest.mark.slow
+def test_k24_bench_step_batch_checked():
+    """The exact first 8-root step bench.py times (K24, models/gpu_tree.tree,
+    roots = bench.pick_roots(...)[:8]), checked root by root."""
+    import bench
+    dg = DeviceGraph.rmat(24, 16 << 24, 1, symmetrize=True)
+    oo, _ = dg.offsets()
+    roots = bench.pick_roots(oo, 64, seed=1)[:8]
+    og = _oracle_graph(dg)
+    _check_batch(dg, roots, P.deserialize(os.path.join(ROOT, "models", "gpu_tree.tree")), og)
+    dg.close()
+
+
+@pytest.mark.parametrize("name", ["kron12", "er12", "mesh64", "u1000", "unreach", "star7"])
+def test_reached_edges_and_level_hist(name):
+    """k_reached (the bench's GTEPS numerator) and k_level_hist (the roofline
+    work model) equal host sums over the golden depths; the instrumented pull
+    scanned-edge counter ES is bracketed by the sequential early-exit scan
+    (a lower bound) and the candidates' total in-degree (an upper bound)."""
+    n, m, a = G.graph_arrays(name)
+    g = P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS])
+    dg = DeviceGraph.upload(g)
+    t = Traversal(dg)
+    od = np.diff(a["out_offsets"].astype(np.int64))
+    idg = np.diff(a["in_offsets"].astype(np.int64))
+    src = a["sources"].astype(np.int64)
+    io = a["in_offsets"].astype(np.int64)
+    try:
+        for r in G.roots(name):
+            want = G.depth(name, r)
+            reach = want != INF
+            counts, _ = t.bfs_full(r, int(P.KernelId.VERTEX_PULL), 2, 32)
+            e, v = t.reached()
+            assert (e, v) == (int(od[reach].sum()), int(reach.sum()))
+            nlev = len(counts)
+            st = t.level_stats(nlev)
+            slot = np.where(reach & (want < nlev), want, nlev)
+            assert st["count"].tolist() == np.bincount(slot, minlength=nlev + 1).tolist()
+            assert st["out_deg"].tolist() == np.bincount(slot, od, minlength=nlev + 1).astype(np.int64).tolist()
+            assert st["in_deg"].tolist() == np.bincount(slot, idg, minlength=nlev + 1).astype(np.int64).tolist()
+            # ES per pull level, instrumented
+            t.instrument(True)
+            for loop in (True, False):
+                t.set_device_loop(loop)
+                t.bfs_full(r, int(P.KernelId.VERTEX_PULL), 2, 32)
+                es = t.level_stats(nlev)["scanned"]
+                rows = np.flatnonzero(idg > 0)
+                pos = np.arange(m, dtype=np.int64) - np.repeat(io[:-1], idg)
+                for lvl in range(nlev):
+                    # sequential early exit: entries scanned up to the first
+                    # in-neighbour at depth lvl (all of them if none)
+                    hitpos = np.where(want[src] == lvl, pos, m)
+                    first = np.minimum.reduceat(hitpos, io[rows]) if rows.size else hitpos[:0]
+                    per = np.where(first < m, first + 1, idg[rows])
+                    cand = want[rows] > lvl                    # unvisited before level lvl
+                    lower = int(per[cand].sum())
+                    upper = int(idg[rows][cand].sum())
+                    assert lower <= int(es[lvl]) <= upper, (name, r, loop, lvl, lower, es[lvl], upper)
+            t.set_device_loop(True)
+            t.instrument(False)
+    finally:
+        t.close()
+        dg.close()

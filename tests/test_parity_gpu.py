@@ -335,3 +335,115 @@ def test_device_tree_cutoffs_match_float64_walk(name):
             np.testing.assert_array_equal(res[True][1], res[False][1])
     finally:
         t.set_device_loop(True)
+
+
+@pytest.mark.parametrize("deg", [1025, 1040, 1057, 2049, 2081, 3000, 5000])
+def test_pull_cta_units_cover_the_in_list_tail(deg):
+    """A pull remainder above kPullHeavy goes to 1024-edge CTA units; the
+    units must cover exactly the unscanned tail.  Vertex `deg` has in-edges
+    from 0..deg-1 and only the LAST one is in the frontier (in-
+    degrees 1024k+1..1024k+33 lost their last in-neighbours)."""
+    src = np.arange(deg, dtype=np.int64)
+    g = P.build_combined(np.stack([src, np.full(deg, deg)], axis=1), deg + 1)
+    root = deg - 1
+    dg = P.DeviceGraph.upload(g)
+    t = P.Traversal(dg)
+    try:
+        for loop in (True, False):
+            t.set_device_loop(loop)
+            for v in P.CountVariant:
+                d = np.empty(g.vertex_count, np.int32)
+                counts, _ = t.bfs_full(root, int(P.KernelId.VERTEX_PULL), int(v), 32, depths_out=d)
+                assert counts.tolist() == [1, 0], (deg, loop, v)
+                assert d[deg] == 1 and d[root] == 0
+        depths = np.full(g.vertex_count, G.INF, np.int32)
+        depths[root] = 0
+        out = P.run_level(g, depths, 0, P.KernelId.VERTEX_PULL, P.CountVariant.DIRECT_ATOMIC)
+        assert out.new_frontier_count == 1 and depths[deg] == 1
+    finally:
+        t.close()
+        dg.close()
+
+
+def test_more_levels_than_megakernel_records():
+    """A traversal with more than 65536 level calls (the megakernel's record
+    capacity) still reports every level: path of 70000."""
+    n = 70000
+    g = P.generate_graph("path", {"n": n}, 0)
+    d, outs = P.bfs_full(g, 0, P.KernelId.VERTEX_PUSH, P.CountVariant.GROUP_REDUCE)
+    assert len(outs) == n
+    assert [o.new_frontier_count for o in outs] == [1] * (n - 1) + [0]
+    np.testing.assert_array_equal(d, np.arange(n, dtype=np.int32))
+    d, tr = P.adaptive_bfs(g, 0, P.tree.leaf_tree(6))
+    assert tr.level_count == n and d[-1] == n - 1
+    assert [r.frontier_size for r in tr.records[-3:]] == [1, 1, 1]
+
+
+def test_concurrent_traversals_on_one_graph():
+    """SPEC.md:243 / SURVEY §8b: distinct traversals may run concurrently on
+    the same immutable Graph.  4 threads x (adaptive_bfs, bfs_full, run_level)
+    on different roots of one Graph; ctypes releases the GIL, so the calls
+    really overlap.  Every result equals the golden vectors."""
+    import threading
+    name = "kron12"
+    g = graph(name)
+    stats = P.compute_stats(g)
+    flat = P.deserialize(G.tree_path("t1"))
+    roots = G.roots(name)
+    tr = G.traces()["small"][name]
+    errors = []
+
+    def worker(i):
+        try:
+            for it in range(6):
+                r = roots[(i + it) % len(roots)]
+                d, trace = P.adaptive_bfs(g, r, flat, stats)
+                np.testing.assert_array_equal(d, G.depth(name, r))
+                got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                       for x in trace.records]
+                assert got == tr[str(r)]["t1"]
+                k, v = P.ALL_PAIRS[(3 * i + it) % 15]
+                d, outs = P.bfs_full(g, r, k, v)
+                np.testing.assert_array_equal(d, G.depth(name, r))
+                assert [o.new_frontier_count for o in outs] == G.counts(name, r).tolist()
+                d = P.init_depths(g, r)
+                for level in range(len(outs)):
+                    P.run_level(g, d, level, k, v)
+                np.testing.assert_array_equal(d, G.depth(name, r))
+        except BaseException as e:   # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+    assert len(g.device_graph()._idle) >= 1   # the pool really handed out extra traversals
+
+
+def test_foreign_graph_upload_cache_is_identity_checked():
+    """kernels._device caches uploads of foreign (reference-shaped) graphs by
+    id with a weak reference; a recycled id never returns another graph."""
+    import gc
+    from types import SimpleNamespace
+
+    from paper_1708_01159_b200 import kernels as K
+
+    class RefGraph(SimpleNamespace):
+        pass
+
+    def mk(name):
+        n, m, a = G.graph_arrays(name)
+        return RefGraph(vertex_count=n, edge_count=m, **{k: a[k] for k in G.ARRAYS})
+
+    for name in ("kron10", "mesh64", "u60", "star7"):
+        fg = mk(name)
+        r = G.roots(name)[0]
+        d, _ = P.bfs_full(fg, r, P.KernelId.VERTEX_PULL, P.CountVariant.GROUP_REDUCE)
+        np.testing.assert_array_equal(d, G.depth(name, r))
+        key = id(fg)
+        assert key in K._foreign_uploads
+        del fg, d
+        gc.collect()
+        assert key not in K._foreign_uploads
