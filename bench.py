@@ -12,8 +12,13 @@ of the K timed steps (CUDA events on the traversal's stream, init_depths
 included).  The graph (8.1 GB of arrays) is larger than L2 and stays
 resident, like model weights.
 
-With N > 1 ranks each GPU holds the graph and takes its own share of the
-roots (multi-source sharding, no data-path collective): scaling "weak".
+With N > 1 ranks (torchrun, one per GPU) the same workload runs as ONE
+tree-switched BFS at a time over a 1-D edge-balanced vertex partition of the
+graph: each rank builds only its slice from the generator
+stream, and the per-level frontier exchange is fused NVLink peer stores
+inside the persistent per-rank megakernel (scaling "strong"); the NCCL
+all-gather exchange and config 3 (Kronecker-26) are secondary keys.
+`--root-sharded` instead replicates the graph and shards the roots.
 
 `--impl reference` times the reference algorithm's CPU port (oracle/, C +
 OpenMP, all host cores) on the same config: the reference is pure Python +
@@ -523,6 +528,213 @@ def run_partitioned(a):
         dist.destroy_process_group()
 
 
+def bench_spec(graph, scale):
+    """Generator spec of the bench graph (configs 2/3: Kronecker; 5: ER; 4: mesh)."""
+    from paper_1708_01159_b200.partition import gen_spec
+    if graph == "er":
+        return gen_spec("uniform", n=1 << 25, edges=1 << 30, seed=1), False, "erdos-renyi-32M-deg32 (directed)"
+    if graph == "mesh":
+        return gen_spec("mesh", rows=4096, cols=4096), True, "mesh-4096x4096"
+    return (gen_spec("rmat", scale=scale, edges=16 << scale, seed=1, symmetrize=True), True,
+            f"kronecker-{scale}-ef16-symmetrised")
+
+
+class PartitionedRun:
+    """One rank of the 1-D partitioned BFS on its own GPU: the
+    slice is built from the generator stream (the whole graph is never on a
+    GPU), the frontier exchange is `exchange` ("peer": fused NVLink peer
+    stores inside the persistent per-rank megakernel; "nccl": NCCL
+    all-gather of the bitmap slices between per-level launches)."""
+
+    def __init__(self, torch, dist, a, graph, scale, exchange, dev):
+        from paper_1708_01159_b200.graph import stats_from_offsets
+        from paper_1708_01159_b200.partition import (DevicePartition, DistExchange,
+                                                     DistPeerExchange, PartitionedBFS,
+                                                     edge_balanced_bounds, gen_offsets, gen_size)
+        self.torch, self.dist = torch, dist
+        rank, world, _ = env_rank()
+        t0 = time.time()
+        self.spec, self.symmetric, self.wname = bench_spec(graph, scale)
+        self.V, self.E = gen_size(self.spec)
+        self.oo, io = gen_offsets(self.spec, dev)          # one streaming degree pass
+        self.stats = stats_from_offsets(self.V, self.E, self.oo, io)
+        self.bounds = edge_balanced_bounds(io, world)
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.stream = torch.cuda.Stream(device=dev)
+        self.part = DevicePartition(None, self.lo, self.hi, self.stream.cuda_stream, spec=self.spec,
+                                    device=dev)
+        self.exch = (DistPeerExchange(torch, dist, self.part) if exchange == "peer"
+                     else DistExchange(torch, dist))
+        self.bfs = PartitionedBFS([self.part], self.bounds, self.exch,
+                                  alloc=lambda s: torch.zeros(s, dtype=torch.int32, device=f"cuda:{dev}"))
+        self.deg_owned = np.diff(self.oo[self.lo:self.hi + 1].astype(np.int64))
+        self.roots = pick_roots(self.oo, 64, seed=1)
+        self.setup_s = time.time() - t0
+        self.exchange = exchange
+
+    def traversed(self, root, flat):
+        """Traversed edges of one tree-switched BFS from root (Σ out-degree of
+        reached vertices, / 2 if symmetric), summed over the ranks' slices."""
+        tr = self.bfs.adaptive(root, flat, self.stats)
+        d = self.part.read_depths()
+        e = float(self.deg_owned[d != 2**31 - 1].sum())
+        t = self.torch.tensor([e], dtype=self.torch.float64,
+                              device="cuda" if self.dist.get_backend() == "nccl" else "cpu")
+        self.dist.all_reduce(t)
+        e = float(t.item())
+        return (e / 2 if self.symmetric else e), tr
+
+    def time_roots(self, order, flat):
+        torch = self.torch
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(self.stream)
+        for r in order:
+            self.bfs.adaptive(r, flat, self.stats)
+        ev1.record(self.stream)
+        torch.cuda.synchronize()
+        return self.exch.max_over_ranks(ev0.elapsed_time(ev1))
+
+    def close(self):
+        self.part.close()
+
+
+def run_multi(a):
+    """--gpus N > 1: one tree-switched BFS at a time over the 1-D
+    edge-balanced vertex partition of the bench graph across the N GPUs
+    (strong scaling of configs[1]'s Kronecker-24 workload; config 3's
+    Kronecker-26 run as a secondary key), fused NVLink peer exchange, with
+    the NCCL all-gather exchange and root-sharded replicas as secondary
+    lines."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1708_01159_b200 as P
+
+    rank, world, local = env_rank()
+    if a.shared_gpu:   # test mode: every rank on GPU 0, gloo control plane, no NCCL line
+        local = 0
+        a.no_secondary = True
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    flat = P.deserialize(a.model)
+    run = PartitionedRun(torch, dist, a, a.graph, a.scale, "peer", local)
+    m_trav, levels = {}, {}
+    for r in run.roots:
+        m_trav[r], tr = run.traversed(r, flat)
+        levels[r] = tr.level_count
+    R = a.roots_per_step
+    order = [run.roots[i % len(run.roots)] for i in range(R * (a.warmup + a.steps))]
+    run.time_roots(order[:R * a.warmup], flat)
+    l0 = run.part.launches()
+    with ClockSampler(local) as clk:
+        ms = run.time_roots(order[R * a.warmup:], flat)
+    launches = run.part.launches() - l0
+    timed = order[R * a.warmup:]
+    edges = sum(m_trav[r] for r in timed)
+    nlev = sum(levels[r] for r in timed)
+    gteps = edges / (ms * 1e-3) / 1e9
+    words = (run.V + 31) // 32
+    recv = int(words * 4 * (world - 1) / world)
+    # e2e: the public partitioned call + the gathered host depth array
+    ne = min(len(run.roots), R)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    e_edges = 0.0
+    for r in run.roots[:ne]:
+        run.bfs.adaptive(r, flat, run.stats)
+        run.bfs.depths()
+        e_edges += m_trav[r]
+    torch.cuda.synchronize()
+    e_el = run.exch.max_over_ranks(time.perf_counter() - t0)
+
+    # ---- secondary: the same BFS with the NCCL all-gather exchange --------
+    nccl = None
+    if not a.no_secondary:
+        from paper_1708_01159_b200.partition import DistExchange, PartitionedBFS
+        nb = PartitionedBFS([run.part], run.bounds, DistExchange(torch, dist),
+                            alloc=lambda s: torch.zeros(s, dtype=torch.int32, device=f"cuda:{local}"))
+        nb.time_exchange = True
+        sample = run.roots[:4]
+        for r in sample[:1]:
+            nb.adaptive(r, flat, run.stats)
+        nb.exchange_ms, nb.exchange_calls = 0.0, 0
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for r in sample:
+            nb.adaptive(r, flat, run.stats)
+        torch.cuda.synchronize()
+        el = run.exch.max_over_ranks(time.perf_counter() - t0)
+        ex_us = run.exch.max_over_ranks(nb.exchange_ms / max(1, nb.exchange_calls)) * 1e3
+        nrecv = (world - 1) * nb.stride * 4
+        nccl = {"gteps": round(sum(m_trav[r] for r in sample) / el / 1e9, 3),
+                "basis": "host wall clock of per-level launches + NCCL all_gather_into_tensor",
+                "mean_allgather_us": round(ex_us, 2),
+                "bytes_received_per_rank_per_level": int(nrecv),
+                "GBps_received_per_rank": round(nrecv / (ex_us * 1e-6) / 1e9, 2) if ex_us else None,
+                "nvlink_peak_GBps_per_direction": 900.0, "roots": len(sample)}
+
+    # ---- secondary: config 3 (Kronecker-26) over the same partition -------
+    k26 = None
+    if not a.no_secondary and a.graph == "kronecker" and a.scale != 26:
+        run.close()
+        r26 = PartitionedRun(torch, dist, a, "kronecker", 26, "peer", local)
+        m26 = {r: r26.traversed(r, flat)[0] for r in r26.roots[:4]}
+        o26 = [r26.roots[i % 4] for i in range(8)]
+        ms26 = r26.time_roots(o26, flat)
+        k26 = {"workload": r26.wname, "vertices": r26.V, "directed_edge_slots": r26.E,
+               "gteps": round(sum(m26[r] for r in o26) / (ms26 * 1e-3) / 1e9, 3),
+               "ms_per_bfs": round(ms26 / len(o26), 4), "bfs_timed": len(o26),
+               "setup_s": round(r26.setup_s, 1)}
+        r26.close()
+    else:
+        run.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (device-generated, bit-exact to the reference generator)",
+            "config": {"workload": f"{run.wname} tree-switched BFS, 1-D vertex partition over "
+                                   f"{world} GPUs",
+                       "graph": a.graph, "scale": a.scale, "vertices": run.V,
+                       "directed_edge_slots": run.E, "roots_per_step": R, "roots_pool": 64,
+                       "step": f"{R} tree-switched BFSs, one at a time over all ranks (one "
+                               "persistent per-rank launch each)",
+                       "parallelism": f"1-D edge-balanced destination partition, {world} ranks x 1 GPU; "
+                                      "per-level frontier exchange = fused NVLink peer stores + "
+                                      "mailbox signal inside the per-rank megakernel",
+                       "slices": "built per rank from the generator stream (whole graph never resident)",
+                       "model": os.path.relpath(a.model, ROOT),
+                       "l2": "inputs larger than L2"},
+            "gpu_launches": int(launches),
+            "exchange": {"kind": "fused peer stores over NVLink (CUDA IPC) + mailbox arrival counters",
+                         "bytes_received_per_rank_per_level": recv,
+                         "levels_timed": nlev,
+                         "nvlink_peak_GBps_per_direction": 900.0,
+                         "nccl_allgather_line": nccl},
+            "config3_k26": k26,
+            "roofline": None,
+            "cpu_baseline": None,
+            "e2e": {"value": round(e_edges / e_el / 1e9, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * ne, "d2h_bytes_per_step": int(4 * run.V * ne),
+                    "api": "PartitionedBFS.adaptive + depths() (gathered host int32 depths)",
+                    "bfs_per_sample": ne},
+            "clocks": clk.summary(),
+            "setup_s": round(run.setup_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def cpu_baseline(dg, roots, model, static24, budget_s, symmetric=True):
     """The reference algorithm's CPU port (oracle/) on the host cores, same
     graph / tree / roots, bounded to ~budget_s seconds (>= 1 root)."""
@@ -629,6 +841,14 @@ def main():
                     help="--partition frontier exchange: fused peer stores or NCCL all-gather")
     ap.add_argument("--virtual-parts", type=int, default=8,
                     help="--partition at N=1: partitions sharing the one GPU")
+    ap.add_argument("--root-sharded", action="store_true",
+                    help="N > 1: replicate the graph and shard the roots (no exchange) instead of "
+                         "the 1-D partitioned BFS")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="N > 1 test mode: all ranks on GPU 0 (gloo control plane; the peer "
+                         "exchange still runs through CUDA IPC)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="N > 1: skip the NCCL-exchange and Kronecker-26 secondary lines")
     ap.add_argument("--mode", type=int, default=1,
                     help="1: device-resident level loop (megakernel); 0: per-level launches")
     a = ap.parse_args()
@@ -641,6 +861,8 @@ def main():
         run_reference(a)
     elif a.partition:
         run_partitioned(a)
+    elif env_rank()[1] > 1 and not a.root_sharded:
+        run_multi(a)
     else:
         run_ours(a)
 

@@ -228,6 +228,41 @@ ABFS_API int abfs_reached_edges(abfs_traversal *t, uint64_t *edges, uint64_t *ve
  * (kernels.py:340-353) restricted to owned destinations. */
 typedef struct abfs_part abfs_part;
 ABFS_API int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part **out);
+
+/* A generator description (the device generators above as data), so a rank
+ * can build its slice without the whole graph ever being on its GPU. */
+enum { ABFS_GEN_RMAT = 0, ABFS_GEN_UNIFORM = 1, ABFS_GEN_MESH = 2 };
+typedef struct abfs_gen_spec {
+    int32_t kind;            /* ABFS_GEN_* */
+    int32_t symmetrize;      /* rmat: append the reversed pairs */
+    uint32_t scale;          /* rmat: |V| = 2^scale */
+    uint32_t rows, cols;     /* mesh */
+    uint64_t n;              /* uniform: |V| (power of two) */
+    uint64_t edges;          /* rmat / uniform: generated pairs */
+    double a, b, c;          /* rmat quadrant probabilities */
+    uint64_t pcg_state[2], pcg_inc[2];
+} abfs_gen_spec;
+/* |V| and |E| (directed slots) of the graph the spec generates. */
+ABFS_API int abfs_gen_size(const abfs_gen_spec *spec, uint64_t *n, uint64_t *m);
+/* Out-/in-degree of every vertex of the generated graph (host arrays of
+ * |V| u32; in_deg may be NULL for a symmetrised spec) from one streaming
+ * pass of the generator on `device` (O(|V|) device memory, no edge arrays):
+ * the inputs of compute_stats (graph.py:180-208) and of the edge-balanced
+ * partition bounds. */
+ABFS_API int abfs_gen_degrees(int device, const abfs_gen_spec *spec, uint32_t *out_deg,
+                              uint32_t *in_deg);
+/* abfs_part_create for the graph `spec` generates, built on `device` from
+ * the generator stream filtered to destinations in [lo, hi): peak device
+ * memory ~ 2 x 8 bytes per owned in-edge plus the slice itself, never the
+ * whole graph.  The slice's arrays equal abfs_part_create's on the full
+ * graph (tests compare them with abfs_part_download). */
+ABFS_API int abfs_part_create_generated(int device, const abfs_gen_spec *spec, uint64_t lo,
+                                        uint64_t hi, abfs_part **out);
+/* Copy a slice's arrays back (tests): fo_off [|V|+1], fo_dst/fo_org [m_fwd],
+ * r_off [hi-lo+1], r_src/r_own [m_rev], r_first [hi-lo]; NULL skips one. */
+ABFS_API int abfs_part_download(const abfs_part *p, uint32_t *fo_off, uint32_t *fo_dst,
+                                uint32_t *fo_org, uint32_t *r_off, uint32_t *r_src,
+                                uint32_t *r_own, uint32_t *r_first);
 ABFS_API void abfs_part_destroy(abfs_part *p);
 ABFS_API int abfs_part_info(const abfs_part *p, uint64_t *lo, uint64_t *hi, uint64_t *m_fwd,
                             uint64_t *m_rev);

@@ -34,6 +34,15 @@ class AbfsTree(ctypes.Structure):
                 ("lefts", u32p), ("rights", u32p), ("leaf_classes", u8p)]
 
 
+class AbfsGenSpec(ctypes.Structure):
+    """abfs_gen_spec (include/abfs.h): a device generator as data."""
+    _fields_ = [("kind", ctypes.c_int32), ("symmetrize", ctypes.c_int32),
+                ("scale", ctypes.c_uint32), ("rows", ctypes.c_uint32), ("cols", ctypes.c_uint32),
+                ("n", ctypes.c_uint64), ("edges", ctypes.c_uint64),
+                ("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double),
+                ("pcg_state", ctypes.c_uint64 * 2), ("pcg_inc", ctypes.c_uint64 * 2)]
+
+
 class AbfsLevelRecord(ctypes.Structure):
     _fields_ = [("level", ctypes.c_int64), ("kernel", ctypes.c_int32),
                 ("variant", ctypes.c_int32), ("fallback", ctypes.c_int32),
@@ -107,6 +116,12 @@ _SIGNATURES = {
     "abfs_features": (ctypes.c_int, [f64p, ctypes.c_uint64, ctypes.c_uint64, f64p]),
     "abfs_part_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, vpp]),
     "abfs_part_destroy": (None, [ctypes.c_void_p]),
+    "abfs_gen_size": (ctypes.c_int, [ctypes.POINTER(AbfsGenSpec), u64p, u64p]),
+    "abfs_gen_degrees": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(AbfsGenSpec), u32p, u32p]),
+    "abfs_part_create_generated": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(AbfsGenSpec),
+                                                  ctypes.c_uint64, ctypes.c_uint64, vpp]),
+    "abfs_part_download": (ctypes.c_int, [ctypes.c_void_p, u32p, u32p, u32p, u32p, u32p, u32p,
+                                          u32p]),
     "abfs_part_info": (ctypes.c_int, [ctypes.c_void_p, u64p, u64p, u64p, u64p]),
     "abfs_part_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "abfs_part_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),

@@ -59,4 +59,16 @@ struct abfs_graph {
 namespace abfs {
 int graph_alloc(abfs_graph *g, uint64_t n, uint64_t m);
 void graph_free(abfs_graph *g);
+
+// One rank's slice of a 1-D partition (partition.cu): the destination-
+// filtered out-CSR over all n sources and the in-CSR rows of the owned range
+// [lo, hi).  gen_slice (graph.cu) builds it from a generator stream; the
+// caller owns the arrays.
+struct Slice {
+    uint64_t mf = 0, mr = 0;
+    uint32_t *fo_off = nullptr, *fo_dst = nullptr, *fo_org = nullptr;
+    uint32_t *r_off = nullptr, *r_src = nullptr, *r_own = nullptr, *r_first = nullptr;
+};
+int gen_slice(int device, const abfs_gen_spec *spec, uint64_t lo, uint64_t hi, Slice &out,
+              uint64_t *n_out, cudaStream_t s);
 }  // namespace abfs

@@ -70,15 +70,12 @@ struct RmatParams {
 
 constexpr int kGenChunk = 16;
 
-__global__ void k_gen_rmat(const RmatParams *__restrict__ P, uint64_t *keys_fwd) {
-    const RmatParams &p = *P;
-    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kGenChunk;
-    if (i0 >= p.m) return;
-    const int cnt = (int)min((uint64_t)kGenChunk, p.m - i0);
+// The scale-bit draws of edges [i0, i0 + cnt) (cnt <= kGenChunk).
+__device__ __forceinline__ void rmat_pairs(const RmatParams &p, uint64_t i0, int cnt,
+                                           uint32_t (&src)[kGenChunk], uint32_t (&dst)[kGenChunk]) {
     u128 A, C;
     pcg_jump(p.inc, (u128)i0, A, C);
     const u128 base = A * p.s0 + C;  // state before draw i0 at bit 0
-    uint32_t src[kGenChunk], dst[kGenChunk];
 #pragma unroll
     for (int k = 0; k < kGenChunk; ++k) src[k] = dst[k] = 0;
     const u128 M = pcg_mult();
@@ -96,6 +93,15 @@ __global__ void k_gen_rmat(const RmatParams *__restrict__ P, uint64_t *keys_fwd)
             }
         }
     }
+}
+
+__global__ void k_gen_rmat(const RmatParams *__restrict__ P, uint64_t *keys_fwd) {
+    const RmatParams &p = *P;
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kGenChunk;
+    if (i0 >= p.m) return;
+    const int cnt = (int)min((uint64_t)kGenChunk, p.m - i0);
+    uint32_t src[kGenChunk], dst[kGenChunk];
+    rmat_pairs(p, i0, cnt, src, dst);
     for (int k = 0; k < cnt; ++k) {
         keys_fwd[i0 + k] = ((uint64_t)src[k] << 32) | dst[k];
         if (p.symmetrize) keys_fwd[p.m + i0 + k] = ((uint64_t)dst[k] << 32) | src[k];
@@ -512,6 +518,328 @@ extern "C" int abfs_graph_generate_mesh(int device, uint32_t rows, uint32_t cols
     *out = g;
     return finish_build(rc, g, out);
 }
+
+// ---- streaming generation: degrees and destination-filtered slices -----------
+//
+// The generators above materialise the whole key stream (8 bytes per slot)
+// and sort it.  A rank of a 1-D partition needs only the edges whose
+// destination it owns, and compute_stats / the edge-balanced bounds need only
+// the degrees, so these kernels regenerate the same stream (same draws, same
+// pairs) and either count degrees or keep the owned pairs.
+
+namespace {
+
+struct GenArgs {
+    int kind;                     // ABFS_GEN_RMAT / ABFS_GEN_UNIFORM
+    const RmatParams *rp;         // rmat (device copy)
+    UniParams up;                 // uniform
+    uint64_t pairs;               // generated pairs
+    int sym;                      // rmat: each pair also yields (dst, src)
+    // degree mode
+    uint32_t *out_deg, *in_deg;   // in_deg NULL: symmetric (one array)
+    // filter mode: keep (s, d) with lo <= d < hi; keys NULL = count only
+    uint64_t *keys;
+    unsigned long long *cursor;
+    uint32_t lo, hi;
+};
+
+// uniform: the pairs of edges [i0, i0 + cnt): src = u32 stream positions
+// i0.., dst = positions m + i0..; u64 draw k yields positions 2k (low half)
+// and 2k + 1 (high half), as in k_gen_uniform.
+__device__ __forceinline__ void uniform_pairs(const UniParams &p, uint64_t i0,
+                                              uint32_t (&src)[kGenChunk], uint32_t (&dst)[kGenChunk]) {
+    const u128 M = pcg_mult();
+    auto val = [&](uint64_t u32) { return (uint32_t)((u32 << p.n_log2) >> 32); };
+    u128 A, C;
+    pcg_jump(p.inc, (u128)(i0 >> 1), A, C);   // i0 is a multiple of kGenChunk: even
+    u128 s = A * p.s0 + C;
+#pragma unroll
+    for (int k = 0; k < kGenChunk / 2; ++k) {
+        s = s * M + p.inc;
+        const uint64_t o = pcg_out(s);
+        src[2 * k] = val(o & 0xffffffffull);
+        src[2 * k + 1] = val(o >> 32);
+    }
+    const uint64_t j = p.m + i0;
+    pcg_jump(p.inc, (u128)(j >> 1), A, C);
+    s = A * p.s0 + C;
+    const int off = (int)(j & 1);
+    uint32_t hw[kGenChunk + 2];
+#pragma unroll
+    for (int k = 0; k < kGenChunk / 2 + 1; ++k) {
+        s = s * M + p.inc;
+        const uint64_t o = pcg_out(s);
+        hw[2 * k] = val(o & 0xffffffffull);
+        hw[2 * k + 1] = val(o >> 32);
+    }
+#pragma unroll
+    for (int k = 0; k < kGenChunk; ++k) dst[k] = off ? hw[k + 1] : hw[k];
+}
+
+// Warp-aggregated append of this thread's kept pairs (all lanes call).
+__device__ __forceinline__ void append_kept(const GenArgs &a, int nkeep, const uint64_t *kept) {
+    const unsigned lane = threadIdx.x & 31u;
+    unsigned incl = (unsigned)nkeep;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    const unsigned tot = __shfl_sync(kFull, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot) base = atomicAdd(a.cursor, (unsigned long long)tot);
+    base = __shfl_sync(kFull, base, 31);
+    if (a.keys) {
+        const unsigned long long at = base + incl - (unsigned)nkeep;
+        for (int k = 0; k < nkeep; ++k) a.keys[at + k] = kept[k];
+    }
+}
+
+template <bool DEGREES>
+__global__ void __launch_bounds__(256) k_gen_stream(GenArgs a) {
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kGenChunk;
+    const int cnt = i0 < a.pairs ? (int)min((uint64_t)kGenChunk, a.pairs - i0) : 0;
+    uint32_t src[kGenChunk], dst[kGenChunk];
+    if (cnt) {
+        if (a.kind == ABFS_GEN_RMAT) rmat_pairs(*a.rp, i0, cnt, src, dst);
+        else uniform_pairs(a.up, i0, src, dst);
+    }
+    if (DEGREES) {
+        for (int k = 0; k < cnt; ++k) {
+            atomicAdd(a.out_deg + src[k], 1u);
+            if (a.in_deg) atomicAdd(a.in_deg + dst[k], 1u);
+            else if (a.sym) atomicAdd(a.out_deg + dst[k], 1u);   // (dst, src) slot
+            if (a.sym && a.in_deg) {
+                atomicAdd(a.out_deg + dst[k], 1u);
+                atomicAdd(a.in_deg + src[k], 1u);
+            }
+        }
+        return;
+    }
+    uint64_t kept[2 * kGenChunk];
+    int nk = 0;
+    for (int k = 0; k < cnt; ++k) {
+        if (dst[k] >= a.lo && dst[k] < a.hi) kept[nk++] = ((uint64_t)src[k] << 32) | dst[k];
+        if (a.sym && src[k] >= a.lo && src[k] < a.hi) kept[nk++] = ((uint64_t)dst[k] << 32) | src[k];
+    }
+    append_kept(a, nk, kept);
+}
+
+// mesh: vertex v's pairs (v, neighbour) as k_gen_mesh emits them.
+template <bool DEGREES>
+__global__ void __launch_bounds__(256) k_mesh_stream(uint32_t rows, uint32_t cols, GenArgs a) {
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t n = (uint64_t)rows * cols;
+    uint64_t nb[4];
+    int k = 0;
+    if (v < n) {
+        const uint32_t r = (uint32_t)(v / cols), c = (uint32_t)(v % cols);
+        if (r > 0) nb[k++] = v - cols;
+        if (c > 0) nb[k++] = v - 1;
+        if (c + 1 < cols) nb[k++] = v + 1;
+        if (r + 1 < rows) nb[k++] = v + cols;
+    }
+    if (DEGREES) {
+        if (v < n) {
+            a.out_deg[v] = (uint32_t)k;
+            if (a.in_deg) a.in_deg[v] = (uint32_t)k;   // the grid is symmetric
+        }
+        return;
+    }
+    uint64_t kept[4];
+    int nk = 0;
+    for (int i = 0; i < k; ++i)
+        if (nb[i] >= a.lo && nb[i] < a.hi) kept[nk++] = (v << 32) | nb[i];
+    append_kept(a, nk, kept);
+}
+
+__global__ void k_pack_rev_local(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ org,
+                                 uint64_t m, uint32_t lo, uint64_t *keys) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = ((uint64_t)(dst[i] - lo) << 32) | org[i];
+}
+
+__global__ void k_add_u32(uint32_t *x, uint64_t m, uint32_t add) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] += add;
+}
+
+// Host side of a spec: sizes and the kernel arguments (rmat params on the device).
+struct GenPlan {
+    uint64_t n = 0, m = 0;
+    GenArgs a{};
+    RmatParams *dp = nullptr;
+    ~GenPlan() { cudaFree(dp); }
+};
+
+int gen_plan(const abfs_gen_spec *spec, GenPlan &g, bool upload) {
+    if (!spec) return fail(ABFS_EINVAL, "null generator spec");
+    g.a.kind = spec->kind;
+    switch (spec->kind) {
+    case ABFS_GEN_RMAT: {
+        if (spec->scale < 1 || spec->scale > 31) return fail(ABFS_EINVAL, "scale must be in [1, 31]");
+        if (spec->a < 0 || spec->b < 0 || spec->c < 0 || spec->a + spec->b + spec->c > 1.0 + 1e-9)
+            return fail(ABFS_EINVAL, "rmat probabilities must be non-negative and sum to <= 1");
+        g.n = 1ull << spec->scale;
+        g.m = spec->symmetrize ? 2 * spec->edges : spec->edges;
+        g.a.pairs = spec->edges;
+        g.a.sym = spec->symmetrize ? 1 : 0;
+        if (upload) {
+            RmatParams hp;
+            hp.s0 = words_to_u128(spec->pcg_state);
+            hp.inc = words_to_u128(spec->pcg_inc);
+            hp.m = spec->edges;
+            hp.scale = spec->scale;
+            hp.symmetrize = g.a.sym;
+            hp.t1 = thr53(spec->a);
+            hp.t2 = thr53(spec->a + spec->b);
+            hp.t3 = thr53(spec->a + spec->b + spec->c);
+            for (uint32_t bit = 0; bit < spec->scale; ++bit)
+                pcg_jump(hp.inc, (u128)bit * spec->edges, hp.bitA[bit], hp.bitC[bit]);
+            ABFS_CUDA(cudaMalloc(&g.dp, sizeof(RmatParams)));
+            ABFS_CUDA(cudaMemcpy(g.dp, &hp, sizeof(RmatParams), cudaMemcpyHostToDevice));
+            g.a.rp = g.dp;
+        }
+        break;
+    }
+    case ABFS_GEN_UNIFORM:
+        if (spec->n == 0 || (spec->n & (spec->n - 1)) || spec->n > (1ull << 31))
+            return fail(ABFS_EINVAL, "device uniform-random needs a power-of-two n <= 2^31");
+        g.n = spec->n;
+        g.m = spec->edges;
+        g.a.pairs = spec->edges;
+        g.a.up.s0 = words_to_u128(spec->pcg_state);
+        g.a.up.inc = words_to_u128(spec->pcg_inc);
+        g.a.up.n_log2 = (uint64_t)bits_for(spec->n);
+        g.a.up.m = spec->edges;
+        break;
+    case ABFS_GEN_MESH:
+        if (spec->rows < 1 || spec->cols < 1) return fail(ABFS_EINVAL, "mesh needs rows, cols >= 1");
+        g.n = (uint64_t)spec->rows * spec->cols;
+        g.m = 2 * ((uint64_t)spec->rows * (spec->cols - 1) + (uint64_t)(spec->rows - 1) * spec->cols);
+        break;
+    default:
+        return fail(ABFS_EINVAL, "unknown generator kind " + std::to_string(spec->kind));
+    }
+    if (g.n >= (1ull << 32)) return fail(ABFS_EINVAL, "vertex_count must be < 2^32");
+    if (g.m >= (1ull << 32)) return fail(ABFS_EINVAL, "edge_count must be < 2^32 (u32 offsets)");
+    return ABFS_OK;
+}
+
+template <bool DEGREES>
+cudaError_t gen_launch(const abfs_gen_spec *spec, const GenPlan &g, const GenArgs &a, cudaStream_t s) {
+    if (spec->kind == ABFS_GEN_MESH) {
+        if (g.n) k_mesh_stream<DEGREES><<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(spec->rows, spec->cols, a);
+    } else if (a.pairs) {
+        const uint64_t threads = (a.pairs + kGenChunk - 1) / kGenChunk;
+        k_gen_stream<DEGREES><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" int abfs_gen_size(const abfs_gen_spec *spec, uint64_t *n, uint64_t *m) {
+    GenPlan g;
+    ABFS_TRY(gen_plan(spec, g, false));
+    if (n) *n = g.n;
+    if (m) *m = g.m;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_gen_degrees(int device, const abfs_gen_spec *spec, uint32_t *out_deg,
+                                uint32_t *in_deg) {
+    if (!out_deg) return fail(ABFS_EINVAL, "null output");
+    GenPlan g;
+    ABFS_CUDA(cudaSetDevice(device));
+    ABFS_TRY(gen_plan(spec, g, true));
+    uint32_t *dd = nullptr;
+    const uint64_t n = g.n;
+    ABFS_CUDA(cudaMalloc(&dd, 2 * (n ? n : 1) * 4));
+    GenArgs a = g.a;
+    a.out_deg = dd;
+    // symmetric specs (symmetrised rmat, mesh) have in == out: one array
+    const bool sym = spec->kind == ABFS_GEN_MESH || (spec->kind == ABFS_GEN_RMAT && spec->symmetrize);
+    a.in_deg = sym ? nullptr : dd + n;
+    cudaError_t e = cudaMemset(dd, 0, 2 * (n ? n : 1) * 4);
+    if (e == cudaSuccess) e = gen_launch<true>(spec, g, a, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out_deg, dd, n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && in_deg) e = cudaMemcpy(in_deg, sym ? dd : dd + n, n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dd);
+    if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("gen_degrees: ") + cudaGetErrorString(e));
+    return ABFS_OK;
+}
+
+namespace abfs {
+
+int gen_slice(int device, const abfs_gen_spec *spec, uint64_t lo, uint64_t hi, Slice &out,
+              uint64_t *n_out, cudaStream_t s) {
+    GenPlan g;
+    ABFS_CUDA(cudaSetDevice(device));
+    ABFS_TRY(gen_plan(spec, g, true));
+    const uint64_t n = g.n;
+    if (lo > hi || hi > n) return fail(ABFS_EINVAL, "partition range out of bounds");
+    *n_out = n;
+    const uint64_t nv = hi - lo;
+    GenArgs a = g.a;
+    a.lo = (uint32_t)lo;
+    a.hi = (uint32_t)hi;
+    unsigned long long *cur = nullptr, mk = 0;
+    ABFS_CUDA(cudaMalloc(&cur, 8));
+    cudaError_t e = cudaMemsetAsync(cur, 0, 8, s);
+    a.cursor = cur;
+    a.keys = nullptr;   // pass 1: count the owned in-edges
+    if (e == cudaSuccess) e = gen_launch<false>(spec, g, a, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&mk, cur, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    KeyBufs kb;
+    if (e == cudaSuccess) e = cudaMalloc(&kb.a, (mk ? mk : 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kb.b, (mk ? mk : 1) * 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cur, 0, 8, s);
+    a.keys = kb.a;      // pass 2: keep them (any order; sorted below)
+    if (e == cudaSuccess) e = gen_launch<false>(spec, g, a, s);
+    cudaFree(cur);
+    auto A = [&](uint32_t **p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc((void **)p, bytes ? bytes : 4);
+    };
+    out.mf = out.mr = mk;
+    // +16 on every stream array: the edge kernels' bulk copies and pull's
+    // aligned 16-byte reads round the last chunk up
+    A(&out.fo_off, (n + 1) * 4);
+    A(&out.fo_dst, mk * 4 + 16);
+    A(&out.fo_org, mk * 4 + 16);
+    A(&out.r_off, (nv + 1) * 4);
+    A(&out.r_src, mk * 4 + 16);
+    A(&out.r_own, mk * 4 + 16);
+    A(&out.r_first, nv * 4 + 16);
+    if (e != cudaSuccess) return fail(ABFS_ECUDA, std::string("gen_slice: ") + cudaGetErrorString(e));
+    // forward slice: (src, dst) order over all sources
+    ABFS_TRY(sort_keys(kb.a, kb.b, mk, bits_for(n), s));
+    k_split_offsets<<<grid_cap(mk + 1, 256), 256, 0, s>>>(kb.a, mk, n, out.fo_org, out.fo_dst, out.fo_off);
+    ABFS_CUDA(cudaGetLastError());
+    // owned in-rows: (dst - lo, src) order
+    if (mk) {
+        k_pack_rev_local<<<grid_cap(mk, 256), 256, 0, s>>>(out.fo_dst, out.fo_org, mk, (uint32_t)lo, kb.a);
+        ABFS_CUDA(cudaGetLastError());
+    }
+    ABFS_TRY(sort_keys(kb.a, kb.b, mk, bits_for(nv ? nv : 1), s));
+    k_split_offsets<<<grid_cap(mk + 1, 256), 256, 0, s>>>(kb.a, mk, nv, out.r_own, out.r_src, out.r_off);
+    ABFS_CUDA(cudaGetLastError());
+    if (mk) {
+        k_add_u32<<<grid_cap(mk, 256), 256, 0, s>>>(out.r_own, mk, (uint32_t)lo);
+        ABFS_CUDA(cudaGetLastError());
+    }
+    if (nv) {
+        k_first_src<<<grid_cap(nv, 256), 256, 0, s>>>(out.r_off, out.r_src, nv, out.r_first);
+        ABFS_CUDA(cudaGetLastError());
+    }
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    return ABFS_OK;
+}
+
+}  // namespace abfs
 
 // ---- ADGR files on the engine side ---------------------------
 

@@ -301,15 +301,57 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
     delete p;
 }
 
-extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part **out) {
-    if (!g || !out) return fail(ABFS_EINVAL, "null argument");
-    const uint64_t n = g->d.n, m = g->d.m;
+// Traversal state of a partition whose slice arrays are in place: owned
+// depths / visited / in-degree-0 bitmaps, global frontier bitmaps and queue,
+// counters and the peer mailbox.
+static int part_alloc_state(abfs_part *p) {
+    cudaStream_t s = p->stream;
+    cudaError_t e = cudaSuccess;
+    auto A = [&](void **ptr, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(ptr, bytes ? bytes : 4);
+    };
+    const uint64_t wpad = p->nwl + 4;
+    A((void **)&p->depth, (p->nv + 4) * 4);
+    A((void **)&p->visited, wpad * 4);
+    A((void **)&p->vprev, wpad * 4);
+    A((void **)&p->noin, wpad * 4);
+    A((void **)&p->fnext, wpad * 4);
+    A((void **)&p->fbm[0], (p->W + 4) * 4);
+    A((void **)&p->fbm[1], (p->W + 4) * 4);
+    A((void **)&p->q, (p->n + 4) * 4);
+    A((void **)&p->qn, (p->nv + 4) * 4);
+    const uint64_t mx = p->mf > p->mr ? p->mf : p->mr;
+    A((void **)&p->units, (mx / kPushHub + 64) * sizeof(uint2));   // see traversal ucap
+    A((void **)&p->dctr, sizeof(Ctr));
+    A((void **)&p->dmb, sizeof(Mailbox));
+    A((void **)&p->dres, 2 * sizeof(unsigned long long));
+    A((void **)&p->box, sizeof(PeerBox));
+    A((void **)&p->pack_ticket, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->box, 0, sizeof(PeerBox), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->pack_ticket, 0, sizeof(unsigned int), s);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&p->hres, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s);
+    if (e == cudaSuccess && p->nwl) {
+        k_part_noin<<<grid_for(p->nwl, kBlock, 148 * 64), kBlock, 0, s>>>(p->r_off, p->nv, p->nwl, p->noin);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventCreate(&p->e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&p->e1);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error(std::string("part_create: ") + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA;
+    }
+    return ABFS_OK;
+}
+
+static int part_new(int device, uint64_t n, uint64_t lo, uint64_t hi, abfs_part **out) {
     if (lo > hi || hi > n) return fail(ABFS_EINVAL, "partition range out of bounds");
     if (lo % 32) return fail(ABFS_EINVAL, "partition start must be a multiple of 32");
     if (hi % 32 && hi != n) return fail(ABFS_EINVAL, "partition end must be a multiple of 32 or |V|");
-    ABFS_CUDA(cudaSetDevice(g->device));
+    ABFS_CUDA(cudaSetDevice(device));
     abfs_part *p = new abfs_part();
-    p->device = g->device;
+    p->device = device;
     p->n = n;
     p->lo = lo;
     p->hi = hi;
@@ -318,8 +360,22 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
     p->whi = (hi + 31) / 32;
     p->nwl = p->whi - p->wlo;
     p->W = (n + 31) / 32;
-    cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) p->own_stream = true;
+    const cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete p;
+        return fail(ABFS_ECUDA, std::string("part_create: ") + cudaGetErrorString(e));
+    }
+    p->own_stream = true;
+    *out = p;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_part **out) {
+    if (!g || !out) return fail(ABFS_EINVAL, "null argument");
+    const uint64_t n = g->d.n, m = g->d.m;
+    abfs_part *p = nullptr;
+    ABFS_TRY(part_new(g->device, n, lo, hi, &p));
+    cudaError_t e = cudaSuccess;
     cudaStream_t s = p->stream;
     auto A = [&](void **ptr, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(ptr, bytes ? bytes : 4);
@@ -377,41 +433,65 @@ extern "C" int abfs_part_create(abfs_graph *g, uint64_t lo, uint64_t hi, abfs_pa
                                                                              p->r_off);
         e = cudaGetLastError();
     }
-    // ---- traversal state ---------------------------------------------------
-    const uint64_t wpad = p->nwl + 4;
-    A((void **)&p->depth, (p->nv + 4) * 4);
-    A((void **)&p->visited, wpad * 4);
-    A((void **)&p->vprev, wpad * 4);
-    A((void **)&p->noin, wpad * 4);
-    A((void **)&p->fnext, wpad * 4);
-    A((void **)&p->fbm[0], (p->W + 4) * 4);
-    A((void **)&p->fbm[1], (p->W + 4) * 4);
-    A((void **)&p->q, (n + 4) * 4);
-    A((void **)&p->qn, (p->nv + 4) * 4);
-    const uint64_t mx = p->mf > p->mr ? p->mf : p->mr;
-    A((void **)&p->units, (mx / kPushHub + 64) * sizeof(uint2));   // see traversal ucap
-    A((void **)&p->dctr, sizeof(Ctr));
-    A((void **)&p->dmb, sizeof(Mailbox));
-    A((void **)&p->dres, 2 * sizeof(unsigned long long));
-    A((void **)&p->box, sizeof(PeerBox));
-    A((void **)&p->pack_ticket, sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemsetAsync(p->box, 0, sizeof(PeerBox), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p->pack_ticket, 0, sizeof(unsigned int), s);
-    if (e == cudaSuccess) e = cudaMallocHost((void **)&p->hres, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s);
-    if (e == cudaSuccess && p->nwl) {
-        k_part_noin<<<grid_for(p->nwl, kBlock, 148 * 64), kBlock, 0, s>>>(p->r_off, p->nv, p->nwl, p->noin);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaEventCreate(&p->e0);
-    if (e == cudaSuccess) e = cudaEventCreate(&p->e1);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         set_error(std::string("part_create: ") + cudaGetErrorString(e));
         abfs_part_destroy(p);
         return e == cudaErrorMemoryAllocation ? ABFS_ENOMEM : ABFS_ECUDA;
     }
+    const int rc = part_alloc_state(p);
+    if (rc != ABFS_OK) {
+        abfs_part_destroy(p);
+        return rc;
+    }
     *out = p;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_create_generated(int device, const abfs_gen_spec *spec, uint64_t lo,
+                                          uint64_t hi, abfs_part **out) {
+    if (!spec || !out) return fail(ABFS_EINVAL, "null argument");
+    uint64_t n = 0;
+    ABFS_TRY(abfs_gen_size(spec, &n, nullptr));
+    abfs_part *p = nullptr;
+    ABFS_TRY(part_new(device, n, lo, hi, &p));
+    Slice sl;
+    int rc = gen_slice(device, spec, lo, hi, sl, &n, p->stream);
+    p->fo_off = sl.fo_off;
+    p->fo_dst = sl.fo_dst;
+    p->fo_org = sl.fo_org;
+    p->r_off = sl.r_off;
+    p->r_src = sl.r_src;
+    p->r_own = sl.r_own;
+    p->r_first = sl.r_first;
+    p->mf = sl.mf;
+    p->mr = sl.mr;
+    if (rc == ABFS_OK) rc = part_alloc_state(p);
+    if (rc != ABFS_OK) {
+        abfs_part_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_part_download(const abfs_part *p, uint32_t *fo_off, uint32_t *fo_dst,
+                                  uint32_t *fo_org, uint32_t *r_off, uint32_t *r_src,
+                                  uint32_t *r_own, uint32_t *r_first) {
+    if (!p) return fail(ABFS_EINVAL, "null partition");
+    std::lock_guard<std::recursive_mutex> _abfs_guard(p->mu);
+    ABFS_CUDA(cudaSetDevice(p->device));
+    ABFS_CUDA(cudaStreamSynchronize(p->stream));
+    auto down = [&](uint32_t *h, const uint32_t *d, uint64_t cnt) -> cudaError_t {
+        if (!h || !cnt) return cudaSuccess;
+        return cudaMemcpy(h, d, cnt * 4, cudaMemcpyDeviceToHost);
+    };
+    ABFS_CUDA(down(fo_off, p->fo_off, p->n + 1));
+    ABFS_CUDA(down(fo_dst, p->fo_dst, p->mf));
+    ABFS_CUDA(down(fo_org, p->fo_org, p->mf));
+    ABFS_CUDA(down(r_off, p->r_off, p->nv + 1));
+    ABFS_CUDA(down(r_src, p->r_src, p->mr));
+    ABFS_CUDA(down(r_own, p->r_own, p->mr));
+    ABFS_CUDA(down(r_first, p->r_first, p->nv));
     return ABFS_OK;
 }
 

@@ -72,19 +72,77 @@ def word_bounds(bounds: np.ndarray) -> np.ndarray:
     return w.astype(np.uint64)
 
 
-class DevicePartition:
-    """One rank's slice on its GPU (`abfs_part`, include/abfs.h)."""
+# ---- generator specs: a rank builds its slice without the whole graph -------
 
-    def __init__(self, dgraph, lo: int, hi: int, stream_ptr: int | None = None):
+def gen_spec(kind: str, **kw) -> L.AbfsGenSpec:
+    """An `abfs_gen_spec` for the device generators (DeviceGraph.rmat /
+    .uniform / .mesh take the same parameters):
+    gen_spec("rmat", scale=, edges=, seed=, symmetrize=, a=.57, b=.19, c=.19),
+    gen_spec("uniform", n=, edges=, seed=), gen_spec("mesh", rows=, cols=)."""
+    from .engine import pcg_words
+    sp = L.AbfsGenSpec()
+    if kind == "rmat":
+        sp.kind, sp.scale, sp.edges = 0, int(kw["scale"]), int(kw["edges"])
+        sp.symmetrize = int(bool(kw.get("symmetrize", False)))
+        sp.a, sp.b, sp.c = kw.get("a", 0.57), kw.get("b", 0.19), kw.get("c", 0.19)
+    elif kind == "uniform":
+        sp.kind, sp.n, sp.edges = 1, int(kw["n"]), int(kw["edges"])
+    elif kind == "mesh":
+        sp.kind, sp.rows, sp.cols = 2, int(kw["rows"]), int(kw["cols"])
+        return sp
+    else:
+        raise ValueError(f"unknown generator {kind!r}")
+    st, inc = pcg_words(int(kw["seed"]))
+    sp.pcg_state[0], sp.pcg_state[1] = int(st[0]), int(st[1])
+    sp.pcg_inc[0], sp.pcg_inc[1] = int(inc[0]), int(inc[1])
+    return sp
+
+
+def gen_size(spec: L.AbfsGenSpec) -> tuple[int, int]:
+    n, m = ctypes.c_uint64(), ctypes.c_uint64()
+    L.check(L.lib().abfs_gen_size(ctypes.byref(spec), ctypes.byref(n), ctypes.byref(m)), "gen_size")
+    return n.value, m.value
+
+
+def gen_offsets(spec: L.AbfsGenSpec, device: int = 0):
+    """(out_offsets, in_offsets) of the generated graph from one streaming
+    degree pass on `device` (no edge arrays): compute_stats's and
+    edge_balanced_bounds's inputs."""
+    n, m = gen_size(spec)
+    od, id_ = np.empty(n, np.uint32), np.empty(n, np.uint32)
+    L.check(L.lib().abfs_gen_degrees(device, ctypes.byref(spec), L.ptr(od, L.u32p),
+                                     L.ptr(id_, L.u32p)), "gen_degrees")
+    oo, io = np.zeros(n + 1, np.uint32), np.zeros(n + 1, np.uint32)
+    np.cumsum(od, out=oo[1:], dtype=np.uint32)
+    np.cumsum(id_, out=io[1:], dtype=np.uint32)
+    if int(oo[-1]) != m or int(io[-1]) != m:
+        raise RuntimeError(f"degree pass counted {int(oo[-1])}/{int(io[-1])} slots, expected {m}")
+    return oo, io
+
+
+class DevicePartition:
+    """One rank's slice on its GPU (`abfs_part`, include/abfs.h): cut from a
+    DeviceGraph, or (``spec=``) built straight from the generator stream on
+    ``device`` without the whole graph ever being resident."""
+
+    def __init__(self, dgraph, lo: int, hi: int, stream_ptr: int | None = None, *,
+                 spec: L.AbfsGenSpec | None = None, device: int | None = None):
         self.lo, self.hi = int(lo), int(hi)
-        self.device = dgraph.device
         self._h = ctypes.c_void_p()
-        L.check(L.lib().abfs_part_create(dgraph._h, self.lo, self.hi, ctypes.byref(self._h)),
-                "part_create")
+        if spec is not None:
+            self.device = int(device or 0)
+            L.check(L.lib().abfs_part_create_generated(self.device, ctypes.byref(spec), self.lo,
+                                                       self.hi, ctypes.byref(self._h)),
+                    "part_create_generated")
+        else:
+            self.device = dgraph.device
+            L.check(L.lib().abfs_part_create(dgraph._h, self.lo, self.hi, ctypes.byref(self._h)),
+                    "part_create")
         mf, mr = ctypes.c_uint64(), ctypes.c_uint64()
         L.check(L.lib().abfs_part_info(self._h, None, None, ctypes.byref(mf), ctypes.byref(mr)),
                 "part_info")
         self.m_fwd, self.m_rev = mf.value, mr.value
+        self.n_total = gen_size(spec)[0] if spec is not None else dgraph.vertex_count
         if stream_ptr is not None:
             self.set_stream(stream_ptr)
 
@@ -160,6 +218,19 @@ class DevicePartition:
         v = ctypes.c_uint64()
         L.check(L.lib().abfs_part_launches(self._h, ctypes.byref(v)), "part_launches")
         return v.value
+
+    def download(self) -> dict:
+        """The slice's arrays on the host (tests)."""
+        n = int(self.n_total)
+        out = {"fo_off": np.empty(n + 1, np.uint32), "fo_dst": np.empty(self.m_fwd, np.uint32),
+               "fo_org": np.empty(self.m_fwd, np.uint32), "r_off": np.empty(self.owned + 1, np.uint32),
+               "r_src": np.empty(self.m_rev, np.uint32), "r_own": np.empty(self.m_rev, np.uint32),
+               "r_first": np.empty(self.owned, np.uint32)}
+        L.check(L.lib().abfs_part_download(self._h, *[L.ptr(out[k], L.u32p) for k in
+                                                      ("fo_off", "fo_dst", "fo_org", "r_off",
+                                                       "r_src", "r_own", "r_first")]),
+                "part_download")
+        return out
 
     def close(self):
         if self._h:
@@ -437,6 +508,6 @@ def local_partitions(dgraph, parts: int, stream_ptr: int | None = None):
     return ps, bounds
 
 
-__all__ = ["ALIGN", "edge_balanced_bounds", "word_bounds", "DevicePartition", "LocalExchange",
+__all__ = ["ALIGN", "gen_spec", "gen_size", "gen_offsets", "edge_balanced_bounds", "word_bounds", "DevicePartition", "LocalExchange",
            "LocalPeerExchange", "DistExchange", "DistPeerExchange", "PartitionedBFS",
            "local_partitions"]

@@ -107,3 +107,22 @@ def test_gloo_world_size_2_matches_golden():
     for rank, status, checked in res:
         assert status == "ok", f"rank {rank}:\n{status}"
         assert checked > 0
+
+
+def test_gen_spec_sizes_and_validation():
+    """abfs_gen_size needs no GPU: |V| / |E| of each generator spec, and the
+    generators' argument errors (graph.py:211-252's configs)."""
+    from paper_1708_01159_b200.partition import gen_size, gen_spec
+    assert gen_size(gen_spec("rmat", scale=24, edges=16 << 24, seed=1, symmetrize=True)) == \
+        (1 << 24, 32 << 24)
+    assert gen_size(gen_spec("rmat", scale=10, edges=1000, seed=1)) == (1024, 1000)
+    assert gen_size(gen_spec("uniform", n=1 << 25, edges=1 << 30, seed=1)) == (1 << 25, 1 << 30)
+    assert gen_size(gen_spec("mesh", rows=4096, cols=4096)) == (4096 * 4096, 2 * 2 * 4096 * 4095)
+    with pytest.raises(ValueError, match="power-of-two"):
+        gen_size(gen_spec("uniform", n=1000, edges=10, seed=1))
+    with pytest.raises(ValueError, match="scale"):
+        gen_size(gen_spec("rmat", scale=0, edges=10, seed=1))
+    with pytest.raises(ValueError, match="2\\^32"):
+        gen_size(gen_spec("rmat", scale=28, edges=16 << 28, seed=1, symmetrize=True))
+    with pytest.raises(ValueError, match="unknown generator"):
+        gen_spec("kron", scale=3)
