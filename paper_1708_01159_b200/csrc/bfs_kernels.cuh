@@ -86,11 +86,19 @@ struct LevelCtx {
     unsigned long long *es;      // optional: in-edges scanned by pull (instrumented runs)
     unsigned long long *work;    // dynamic work cursor of this level (= &ctr->work[out])
     uint32_t pull_light;         // pull phase A: entries each lane scans alone
+    uint32_t *acc;               // non-null: RED-mode top-down claims (candidate bits are
+                                 // OR-ed here fire-and-forget; red_compact_body settles them)
     unsigned long long seq;
     int zero_slot;
     int32_t level;
     int32_t lvl1;
 };
+
+#ifndef ABFS_RED_FILTER
+#define ABFS_RED_FILTER 0   // RED-mode claim filter (A/B on B200, K24 / ER-32M switched GTEPS):
+                            // 0 = visited check only (811 / 889), 1 = + skip bits already pending
+                            // in acc (831 / 816), 2 = warp word dedupe (729 / 564), 3 = both (774 / 615)
+#endif
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
@@ -187,6 +195,42 @@ __device__ __forceinline__ void claim4(const LevelCtx &c, const uint32_t (&v)[4]
     uint32_t wv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) wv[k] = act[k] ? c.visited[v[k] >> 5] : 0xffffffffu;
+    if (c.acc) {
+        // RED mode: no returning atomic, no depth write, no emission here --
+        // the unvisited candidates' bits go to acc with fire-and-forget
+        // reductions and red_compact_body claims them word by word
+#if ABFS_RED_FILTER & 1
+        // skip candidates whose bit is already pending (hub adjacency:
+        // many frontier vertices share neighbours; a RED per duplicate
+        // serialises on the word in L2)
+        uint32_t av[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            av[k] = (act[k] && !(wv[k] & (1u << (v[k] & 31)))) ? __ldcg(c.acc + (v[k] >> 5)) : 0xffffffffu;
+#endif
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t bit = 1u << (v[k] & 31);
+#if ABFS_RED_FILTER & 1
+            bool need = !(av[k] & bit);
+#else
+            bool need = act[k] && !(wv[k] & bit);
+#endif
+#if ABFS_RED_FILTER & 2
+            // one RED per distinct word of the warp instruction
+            const unsigned peers = __match_any_sync(kFull, need ? (v[k] >> 5) : 0xffffffffu);
+            const uint32_t all = __reduce_or_sync(peers, need ? bit : 0u);
+            need = need && lane_id() == (unsigned)(__ffs(peers) - 1);
+#else
+            const uint32_t all = bit;
+#endif
+            if (need)
+                asm volatile("red.global.or.b32 [%0], %1;" ::"l"(c.acc + (v[k] >> 5)), "r"(all)
+                             : "memory");
+            won[k] = false;
+        }
+        return;
+    }
     uint32_t old[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -829,6 +873,85 @@ k_heavy(LevelCtx c, const uint32_t *__restrict__ out_off, const uint32_t *__rest
 }
 
 // ---------------------------------------------------------------------------
+// RED-mode epilogue of a top-down level (megakernel).  The edge phase OR-ed
+// the bits of unvisited candidates into `acc` with fire-and-forget
+// reductions (claim4 with c.acc set); here every bitmap word is settled by
+// exactly one thread: new = acc & ~visited, visited |= new, depth[new] =
+// level + 1, the new vertices are appended to the next queue (the count
+// variant shapes the reservations: DIRECT one global atomic per discovery,
+// GROUP one per warp, TWO_LEVEL one per CTA tile), acc is cleared (it is
+// all-zero between levels), and fbm_out (if given) receives the next
+// frontier bitmap.  The set of discoveries is the same as with per-edge
+// atomic claims: every unvisited vertex with a frontier in-neighbour.
+// ---------------------------------------------------------------------------
+template <int VAR>
+__device__ __forceinline__ void red_compact_body(const LevelCtx &c, uint32_t *acc,
+                                                 uint32_t *fbm_out, uint64_t words,
+                                                 unsigned *warp_tot, unsigned *s_base) {
+    const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+    for (uint64_t w0 = (uint64_t)blockIdx.x * kBlock; w0 < words; w0 += (uint64_t)gridDim.x * kBlock) {
+        const uint64_t w = w0 + threadIdx.x;
+        uint32_t nw = 0;
+        if (w < words) {
+            const uint32_t a = acc[w];
+            if (a) {
+                acc[w] = 0u;
+                const uint32_t vis = c.visited[w];
+                nw = a & ~vis;
+                if (nw) c.visited[w] = vis | nw;
+            }
+            if (fbm_out) fbm_out[w] = nw;
+        }
+        const unsigned cnt = __popc(nw);
+        unsigned pos = 0;
+        if (VAR == 0) {
+            uint32_t x = nw;
+            while (x) {
+                const uint32_t v = (uint32_t)(w * 32 + (__ffs(x) - 1));
+                c.depth[v] = c.lvl1;
+                c.q_next[atomicAdd(c.q_tail, 1u)] = v;
+                x &= x - 1;
+            }
+            continue;
+        }
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        if (VAR == 1) {
+            const unsigned tot = __shfl_sync(kFull, incl, 31);
+            unsigned b = 0;
+            if (lane == 31 && tot) b = atom_add_global(c.q_tail, tot);
+            pos = __shfl_sync(kFull, b, 31) + incl - cnt;
+        } else {
+            if (lane == 31) warp_tot[wid] = incl;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned acc_ = 0;
+                for (int i = 0; i < kWarps; ++i) {
+                    const unsigned t = warp_tot[i];
+                    warp_tot[i] = acc_;
+                    acc_ += t;
+                }
+                *s_base = acc_ ? atomicAdd(c.q_tail, acc_) : 0u;
+            }
+            __syncthreads();
+            pos = *s_base + warp_tot[wid] + incl - cnt;
+            __syncthreads();   // warp_tot / s_base are reused by the next tile
+        }
+        uint32_t x = nw;
+        while (x) {
+            const uint32_t v = (uint32_t)(w * 32 + (__ffs(x) - 1));
+            c.depth[v] = c.lvl1;
+            c.q_next[pos++] = v;
+            x &= x - 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // VERTEX_PULL (run_level_vertex_pull, kernels.py:270-300): unvisited
 // vertices scan their in-neighbours and stop at the first frontier vertex.
 // The CTA takes chunks of 8 sub-tiles (one global atomic), its warps take
@@ -1206,6 +1329,51 @@ __device__ __forceinline__ void bitmap_to_queue_tile(const uint32_t *__restrict_
         const int b = __ffs(w) - 1;
         q[pos++] = (uint32_t)(word * 32 + b);
         w &= w - 1;
+    }
+}
+
+// bitmap -> queue for a persistent grid: CTA b converts the contiguous word
+// range [b*per, (b+1)*per), each thread a contiguous run of its words (loads
+// issued back to back), one CTA scan and ONE queue reservation per CTA (the
+// tile version above makes every CTA walk several 256-word tiles, each with
+// its own barriers and global atomic).
+__device__ __forceinline__ void bitmap_to_queue_grid(const uint32_t *__restrict__ fbm, uint64_t words,
+                                                     uint32_t *q, unsigned int *cursor,
+                                                     unsigned *warp_tot, unsigned *base) {
+    const uint64_t per = (words + gridDim.x - 1) / gridDim.x;
+    const uint64_t b0 = min(words, (uint64_t)blockIdx.x * per), b1 = min(words, b0 + per);
+    const uint64_t K = (per + kBlock - 1) / kBlock;
+    const uint64_t t0 = min(b1, b0 + threadIdx.x * K), t1 = min(b1, t0 + K);
+    unsigned cnt = 0;
+    for (uint64_t w = t0; w < t1; ++w) cnt += __popc(fbm[w]);
+    const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            const unsigned t = warp_tot[i];
+            warp_tot[i] = acc;
+            acc += t;
+        }
+        *base = acc ? atomicAdd(cursor, acc) : 0u;
+    }
+    __syncthreads();
+    unsigned pos = *base + warp_tot[wid] + incl - cnt;
+    __syncthreads();   // warp_tot / base are reused by the caller's next use
+    if (!cnt) return;
+    for (uint64_t w = t0; w < t1; ++w) {
+        uint32_t x = fbm[w];
+        while (x) {
+            q[pos++] = (uint32_t)(w * 32 + (__ffs(x) - 1));
+            x &= x - 1;
+        }
     }
 }
 

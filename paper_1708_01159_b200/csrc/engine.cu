@@ -77,6 +77,7 @@ struct abfs_traversal {
     unsigned long long *mnlev = nullptr, *dnlev = nullptr;   // host-mapped level counts (per root)
     uint32_t *hroots = nullptr, *droots = nullptr;            // batch roots (pinned / device)
     unsigned long long *dsums = nullptr;                     // per-root depth checksums (device)
+    uint32_t *acc = nullptr;                                 // RED-mode candidate bits [words], all-zero between levels
     std::vector<unsigned char> last_blob;                    // tree blob resident on the device
     std::vector<unsigned long long> batch_levels;            // per-root level counts, last launch
     size_t batch_recs = 0;                                   // records kept in mrecs, last launch
@@ -113,6 +114,12 @@ static uint32_t pull_light() {
         if (v < 1) v = 1;
     }
     return v;
+}
+
+// Unsigned tuning knob from the environment (read per call: tests toggle it).
+static uint64_t env_u64(const char *name, uint64_t dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : dflt;
 }
 
 // One level's strategy launch over a StratArgs view (launch.cuh).
@@ -214,6 +221,7 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     const int out = (int)(t->call % 3);
     const unsigned long long seq = ++t->call;
     LevelCtx c;
+    c.acc = nullptr;
     c.depth = t->depth;
     c.visited = t->visited;
     c.fbm = t->fbm[t->cur];
@@ -364,6 +372,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     if (t->hroots) cudaFreeHost(t->hroots);
     cudaFree(t->droots);
     cudaFree(t->dsums);
+    cudaFree(t->acc);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
     if (t->stage) cudaFreeHost(t->stage);
@@ -696,7 +705,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
                                   cudaMemcpyHostToDevice, s));
     }
     ABFS_TRY(ensure_events(t, 2));
-    MegaParams P;
+    MegaParams P{};   // value-initialised: every optional pointer starts null
     P.depth = t->depth;
     P.visited = t->visited;
     P.noin = t->noin;
@@ -750,6 +759,26 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     if (checksums) {
         ABFS_CUDA(cudaMemsetAsync(t->dsums, 0, nroots * sizeof(unsigned long long), s));
         P.checksums = t->dsums;
+    }
+    // RED-mode top-down levels (ABFS_RED=0 disables; ABFS_RED_F / ABFS_RED_UNITS
+    // override the thresholds, e.g. 1 / 1 forces every top-down level).
+    // Measured on B200 (tools/level_ab.py): a full RED level is about as fast
+    // as per-edge atomic claims (the random-address L2 reductions bound both)
+    // but hands the next level a ready frontier bitmap -- ER-32M's pull after
+    // its 18.6 M-discovery push level drops 437 -> 289 us (the queue -> bitmap
+    // conversion it saves scatters one atomic per frontier vertex).  RED on a
+    // hub's CTA units alone is slower (K24 hub level 61 -> 95 us: duplicate
+    // candidates are not filtered by claims made earlier in the level), so
+    // units stay on atomic claims by default.
+    P.acc = nullptr;
+    P.red_frontier = env_u64("ABFS_RED_F", g.n >> 7 > 4096 ? g.n >> 7 : 4096);
+    P.red_units = (uint32_t)env_u64("ABFS_RED_UNITS", 0xffffffffull);
+    if (env_u64("ABFS_RED", 1)) {
+        if (!t->acc) {
+            ABFS_CUDA(cudaMalloc((void **)&t->acc, (t->words + 4) * 4));
+            ABFS_CUDA(cudaMemsetAsync(t->acc, 0, (t->words + 4) * 4, s));
+        }
+        P.acc = t->acc;
     }
     for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
     std::lock_guard<std::mutex> mega_guard(g_mega_mu[t->device & 63]);
@@ -1198,3 +1227,13 @@ extern "C" int abfs_adaptive_bfs_batch_check(abfs_traversal *t, const int64_t *r
     return batch_impl(t, roots, nroots, tr, static24, chunk, levels, nullptr, nullptr, checksums,
                       new_counts, counts_cap, n_counts);
 }
+
+#ifdef ABFS_DIAG_CTA
+// diagnostic build only (tools/diag_cta.py): copy g_diag_cta out
+extern "C" __attribute__((visibility("default"))) int abfs_debug_diag_cta(unsigned long long *out) {
+    ABFS_CUDA(cudaMemcpyFromSymbol(out, abfs::g_diag_cta, sizeof(abfs::g_diag_cta)));
+    static unsigned long long zeros[128 * 1024];
+    ABFS_CUDA(cudaMemcpyToSymbol(abfs::g_diag_cta, zeros, sizeof(zeros)));   // clear for the next run
+    return ABFS_OK;
+}
+#endif

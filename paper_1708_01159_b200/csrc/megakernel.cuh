@@ -85,6 +85,15 @@ struct MegaParams {
     // optional [nroots]: per-root depth checksum (depth_mix) of the final
     // depth array of each traversal, for batch parity checks
     unsigned long long *checksums;
+    // RED-mode top-down levels (single graph only; acc = nullptr disables):
+    // acc [words] all-zero between levels; a push / push-warp level with
+    // frontier >= red_frontier runs its edge phase with fire-and-forget OR
+    // reductions into acc and settles them in one bitmap pass (which also
+    // yields the next frontier bitmap); a level whose light pass queued >=
+    // red_units CTA units runs just the unit pass that way
+    uint32_t *acc;
+    uint64_t red_frontier;
+    uint32_t red_units;
 };
 
 // Order-sensitive checksum term of one vertex's depth (numpy restatement in
@@ -179,12 +188,32 @@ __device__ __forceinline__ int mega_tree_class(const CutNode *T, unsigned long l
     return tc->cls;
 }
 
+#ifdef ABFS_DIAG_CTA
+// diagnostic build only: per level, per CTA, the %globaltimer at the end of
+// the light pass [2*level] and of the CTA-unit pass [2*level+1]
+__device__ unsigned long long g_diag_cta[128 * 1024];
+#define ABFS_DIAG_MARK(slot)                                                                \
+    do {                                                                                    \
+        if (threadIdx.x == 0 && c.level < 64 && blockIdx.x < 1024)                          \
+            g_diag_cta[(2 * c.level + (slot)) * 1024 + blockIdx.x] = globaltimer();         \
+    } while (0)
+#else
+#define ABFS_DIAG_MARK(slot) \
+    do {                     \
+    } while (0)
+#endif
+
+// Returns kStratBitmap if the level also wrote a complete next-frontier
+// bitmap (full RED-mode top-down level).
+constexpr int kStratBitmap = 1;
+
 template <int VAR>
-__device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
-                                              uint32_t F, const uint32_t *q, uint32_t *fbm_next,
-                                              SmemQ *sq, unsigned *sn, int *s_done,
-                                              uint32_t *pfound, unsigned int *sfetch,
-                                              cg::grid_group &grid) {
+__device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx &c, int kernel,
+                                             uint32_t F, const uint32_t *q, uint32_t *fbm_next,
+                                             SmemQ *sq, unsigned *sn, int *s_done,
+                                             uint32_t *pfound, unsigned int *sfetch,
+                                             unsigned *warp_tot, unsigned *s_base,
+                                             cg::grid_group &grid) {
     // Two-phase strategies (light pass, then CTA work units) need a second
     // barrier only if the light pass created units: after the first barrier
     // every CTA reads the same unit count, and with none the level's count
@@ -198,11 +227,26 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
         edge_body<VAR, true, 1>(c, sq, P.rev_owner, P.src, P.m_rev);
         break;
     case 2:
-        push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, gridDim.x);
+    case 4: {
+        if (kernel == 2) push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, gridDim.x);
+        else push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2, blockIdx.x, gridDim.x);
+        ABFS_DIAG_MARK(0);
         grid.sync();
-        if (!units()) return;
-        heavy_body<VAR>(c, sq, P.out_off, P.dst, blockIdx.x, gridDim.x);
-        break;
+        const unsigned nu = units();
+        if (!c.acc && !nu) return 0;
+        // a heavy unit pass goes RED too once it is big enough
+        LevelCtx cu = c;
+        if (!cu.acc && P.acc && nu >= P.red_units) cu.acc = P.acc;
+        if (nu) {
+            heavy_body<VAR>(cu, sq, P.out_off, P.dst, blockIdx.x, gridDim.x);
+            ABFS_DIAG_MARK(1);
+            grid.sync();
+        }
+        if (!cu.acc) return 0;
+        red_compact_body<VAR>(c, cu.acc, c.acc ? fbm_next : nullptr, P.words, warp_tot, s_base);
+        grid.sync();
+        return c.acc ? kStratBitmap : 0;
+    }
     case 3:
         {
             // the pull scratch lists alias the (idle) CTA queue buffer
@@ -211,18 +255,15 @@ __device__ __forceinline__ void mega_strategy(const MegaParams &P, const LevelCt
             pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, P.wlo, P.wend,
                            sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
         }
+        ABFS_DIAG_MARK(0);
         grid.sync();
-        if (!units()) return;
+        if (!units()) return 0;
         pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
         break;
-    default:
-        push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2, blockIdx.x, gridDim.x);
-        grid.sync();
-        if (!units()) return;
-        heavy_body<VAR>(c, sq, P.out_off, P.dst, blockIdx.x, gridDim.x);
-        break;
     }
+    ABFS_DIAG_MARK(1);
     grid.sync();
+    return 0;
 }
 
 // One top-down level's light pass on cluster 0 (solo mode).
@@ -356,6 +397,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                         P.ctr->work[z] = 0;
                     }
                     LevelCtx sc;
+                    sc.acc = nullptr;
                     sc.depth = P.depth;
                     sc.visited = P.visited;
                     sc.fbm = cur ? P.fbm1 : P.fbm0;
@@ -490,10 +532,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         const bool need_queue = (pk == 2 || pk == 4);
         int conv = 0;
         if (need_queue && !has_q) {          // bitmap -> queue (switch cost)
-            for (uint64_t w0 = (uint64_t)blockIdx.x * kBlock; w0 < P.words;
-                 w0 += (uint64_t)gridDim.x * kBlock)
-                bitmap_to_queue_tile(fbm_cur, P.words, w0, q_cur, &P.ctr->cq3[out], warp_tot,
-                                     &s_base);
+            bitmap_to_queue_grid(fbm_cur, P.words, q_cur, &P.ctr->cq3[out], warp_tot, &s_base);
             grid.sync();
             has_q = true;
             conv = 1;
@@ -526,15 +565,19 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
         c.work = &P.ctr->work[out];
         c.pull_light = P.pull_light;
+        // RED-mode top-down level (single graph, big frontier): the same for
+        // every CTA (depends on the level's pair and frontier only)
+        c.acc = (need_queue && P.acc && frontier >= P.red_frontier) ? P.acc : nullptr;
         c.seq = 0;
         c.zero_slot = zero;
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
         uint32_t *pull_next = P.part ? P.fnext : fbm_nxt;
+        int sflags;
         switch (pv) {
-        case 0: mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
-        case 1: mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
-        default: mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, grid); break;
+        case 0: sflags = mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
+        case 1: sflags = mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
+        default: sflags = mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
         }
         const bool topdown = pk != 3;
         unsigned long long nw;
@@ -619,7 +662,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         discovered += nw;
         cur ^= 1;
         has_q = P.part ? false : topdown;   // a partition's next frontier is the gathered bitmap
-        has_bm = P.part ? true : !topdown;
+        has_bm = P.part ? true : (!topdown || (sflags & kStratBitmap));
     }
     if (P.checksums) {
         // the traversal's last level ended at a grid barrier: every depth is final

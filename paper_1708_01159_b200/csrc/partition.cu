@@ -553,6 +553,7 @@ static int part_strategy(abfs_part *p, int64_t level, int kernel, int variant, i
     const int out = (int)(p->call % 3);
     const unsigned long long seq = ++p->call;
     LevelCtx c;
+    c.acc = nullptr;
     c.depth = p->depth - p->lo;          // rebased: indexed by global id in [lo, hi)
     c.visited = p->visited - p->wlo;
     c.fbm = p->fbm[p->cur];
@@ -943,7 +944,7 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     ABFS_CUDA(cudaMemcpy(p->droots, &r32, 4, cudaMemcpyHostToDevice));
     ABFS_CUDA(cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s));
     ABFS_CUDA(cudaMemsetAsync(&p->box->timeout, 0, sizeof(unsigned int), s));
-    MegaParams P;
+    MegaParams P{};   // value-initialised: every optional pointer starts null
     std::memset(&P, 0, sizeof(P));
     P.depth = p->depth - p->lo;
     P.visited = p->visited - p->wlo;
@@ -994,6 +995,8 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     P.xcount = p->dx;
     P.gcount = p->dx + 1;
     P.xseq0 = p->p2p_seq;
+    P.checksums = nullptr;
+    P.acc = nullptr;   // RED-mode levels are single-graph only
     *(volatile unsigned long long *)p->mnlev = 0;
     {
         std::lock_guard<std::mutex> mega_guard(mega_mutex(p->device));

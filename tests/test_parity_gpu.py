@@ -447,3 +447,60 @@ def test_foreign_graph_upload_cache_is_identity_checked():
         del fg, d
         gc.collect()
         assert key not in K._foreign_uploads
+
+
+@pytest.fixture(params=[("1", "1"), ("1000000000000", "1")], ids=["red-every-level", "red-units-only"])
+def red_mode(request, monkeypatch):
+    """Force the megakernel's RED-mode top-down claims (fire-and-forget OR
+    reductions + one bitmap settle pass) onto small graphs: on every top-down
+    level, or only on CTA-unit passes (read per call by the engine)."""
+    f, u = request.param
+    monkeypatch.setenv("ABFS_RED_F", f)
+    monkeypatch.setenv("ABFS_RED_UNITS", u)
+    yield request.param
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_red_mode_all_pairs_and_traces_match_reference(name, red_mode):
+    g = graph(name)
+    t = g.device_graph().scratch()
+    assert t.mode  # device loop (RED mode lives in the megakernel)
+    stats = P.compute_stats(g)
+    traces = G.traces()["small"]
+    for r in G.roots(name):
+        want = G.depth(name, r)
+        cnt = G.counts(name, r).tolist()
+        for k, v in P.ALL_PAIRS:
+            d, outs = P.bfs_full(g, r, k, v)
+            np.testing.assert_array_equal(d, want, err_msg=f"{name} root={r} {k.name} {v.name}")
+            assert [o.new_frontier_count for o in outs] == cnt, (name, r, k, v)
+        for key, tree in G.trees_for(name):
+            d, tr = P.adaptive_bfs(g, r, P.deserialize(G.tree_path(tree)), stats)
+            got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                   for x in tr.records]
+            assert got == traces[name][str(r)][key], (name, r, key)
+            np.testing.assert_array_equal(d, want)
+
+
+def test_red_mode_batch_checksums_k18(red_mode):
+    """RED mode through the batched launch the bench times: per-root depth
+    checksums and per-level counts equal the oracle's on Kronecker-18."""
+    from paper_1708_01159_b200 import DeviceGraph, Traversal
+    from paper_1708_01159_b200.engine import depth_checksum
+    from paper_1708_01159_b200.features import static_vector
+    dg = DeviceGraph.rmat(18, 16 << 18, 1, symmetrize=True)
+    g = dg.to_graph()
+    og = oracle.OracleGraph.from_graph(g)
+    flat = P.deserialize(G.tree_path("t1"))
+    t = Traversal(dg)
+    deg = np.diff(g.out_offsets.astype(np.int64))
+    roots = [int(x) for x in np.flatnonzero(deg > 0)[[0, 7, 1000, 5000]]]
+    lv, sums, per = t.adaptive_batch_check(roots, flat.as_abfs(),
+                                           static_vector(P.compute_stats(g)))
+    for i, r in enumerate(roots):
+        want = oracle.reference_bfs(og, r)
+        assert int(sums[i]) == depth_checksum(want), r
+        n = int(lv[i])
+        hist = np.bincount(want[want != G.INF], minlength=n)
+        assert per[i] == hist[1:n].tolist() + [0], r
+    t.close()
