@@ -61,6 +61,8 @@ struct Ctr {
     unsigned int pad2;
     unsigned long long es3[3];   // megakernel: per-level pull scanned edges
     unsigned long long work[3];  // per-level dynamic work cursors
+    unsigned int ps[3];          // megakernel pull: survivor-list tails
+    unsigned int pc[3];          // megakernel pull: carried-candidate-list tails
 };
 
 // Host-mapped result of the last level (written by the device).
@@ -417,6 +419,15 @@ struct CEmit {
             if ((mask >> lane_id()) & 1u) atomicAdd(count, 1ull);
         } else {
             acc += __popc(mask);
+        }
+    }
+
+    // per-lane discovery counts (all lanes call)
+    __device__ __forceinline__ void add_n(unsigned n) {
+        if (VAR == 0) {
+            if (n) atomicAdd(count, (unsigned long long)n);
+        } else {
+            acc += __reduce_add_sync(kFull, n);
         }
     }
 
@@ -990,7 +1001,7 @@ constexpr int kPullChunkSubs = ABFS_PULL_CHUNK;  // sub-tiles per CTA chunk fetc
 // so the fetch is a native shared atomic (a 64-bit one is a CAS loop)
 constexpr uint32_t kFetchInit = 0xfffffeu, kFetchDone = 0xffffffu;
 
-template <int VAR>
+template <int VAR, int G = 1>
 __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ in_off,
                                           const uint32_t *__restrict__ src,
@@ -998,7 +1009,7 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
                                           const uint32_t *__restrict__ noin,
                                           uint32_t *__restrict__ fbm_next, uint64_t word0,
                                           uint64_t words, uint32_t *wbuf, uint32_t *wfound,
-                                          unsigned int *sfetch) {
+                                          unsigned int *sfetch /* [2] */) {
     // words [word0, words) of the bitmaps (a vertex partition passes its
     // owned range; bitmap/offset pointers are indexed by global ids);
     // wbuf = kPullList entries, wfound = kPullSub words, both per warp
@@ -1013,10 +1024,31 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
     // word indices fit 32 bits (|V| < 2^32): 32-bit bookkeeping keeps the
     // megakernel's register pressure down
     const uint32_t w0 = (uint32_t)word0, wend = (uint32_t)words;
+    // G sub-tiles per warp fetch ("unit"): G = 1 on dense levels (fine
+    // grain balances the level's end); G = 4 on sparse levels, where the
+    // sweep is latency-bound -- all 32 lanes load visited / in-degree-0 words
+    // at once (4x the loads in flight) and sub-tiles without candidates cost
+    // nothing more
+    static_assert(G * kPullSub <= 32 && (kPullSub & (kPullSub - 1)) == 0, "pull unit");
     const uint32_t nsub = (wend - w0 + kPullSub - 1) / kPullSub;
-    const uint32_t nchunks = (nsub + kPullChunkSubs - 1) / kPullChunkSubs;
-    if (threadIdx.x == 0) *sfetch = (kFetchInit << 8) | kPullChunkSubs;
+    const uint32_t nunit = (nsub + G - 1) / G;
+    const uint32_t nchunks = (nunit + kPullChunkSubs - 1) / kPullChunkSubs;
+    // sfetch[0] = cursor (chunk id << 8 | next sub-tile), sfetch[1] = the
+    // CTA's NEXT chunk, fetched one chunk ahead: the global atomic's round
+    // trip is paid by the warp that installs a chunk while the other warps
+    // work on it (a refill on demand stalled all 8 warps once per chunk --
+    // most of a sparse pull level's sweep time).  CTA b starts on chunk b;
+    // dynamic chunks are numbered from gridDim on.
+    const uint32_t nblk = gridDim.x;
+    if (threadIdx.x == 0) {
+        sfetch[0] = blockIdx.x < nchunks ? (blockIdx.x << 8) : (kFetchDone << 8);
+        sfetch[1] = kFetchInit;
+    }
     __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < nchunks) {
+        const uint32_t g = nblk + (uint32_t)atomicAdd(c.work, 1ull);
+        *(volatile unsigned int *)(sfetch + 1) = g < nchunks ? g : kFetchDone;
+    }
     unsigned long long scanned = 0;
     for (;;) {
         uint32_t st = 0;
@@ -1024,56 +1056,66 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
         st = __shfl_sync(kFull, st, 0);
         uint32_t cid = st >> 8, sidx = st & 0xffu;
         if (cid == kFetchDone) break;
-        if (sidx > (uint32_t)kPullChunkSubs) {   // another warp is refilling the chunk
+        if (sidx > (uint32_t)kPullChunkSubs) {   // another warp is installing the next chunk
             if (lane == 0)
                 while ((*(volatile unsigned int *)sfetch >> 8) == cid) {
                 }
             __syncwarp();
             continue;
         }
-        if (sidx == (uint32_t)kPullChunkSubs) {  // this warp refills it
-            unsigned long long g = 0;
+        if (sidx == (uint32_t)kPullChunkSubs) {  // this warp installs the prefetched chunk
+            uint32_t g = 0;
             if (lane == 0) {
-                g = atomicAdd(c.work, 1ull);
-                atomicExch(sfetch, g < nchunks ? ((uint32_t)g << 8) | 1u : kFetchDone << 8);
+                while ((g = *(volatile unsigned int *)(sfetch + 1)) == kFetchInit) {
+                }
+                *(volatile unsigned int *)(sfetch + 1) = kFetchInit;
+                atomicExch(sfetch, g != kFetchDone ? (g << 8) | 1u : kFetchDone << 8);
+                if (g != kFetchDone) {   // and fetches the one after it
+                    const uint32_t g2 = nblk + (uint32_t)atomicAdd(c.work, 1ull);
+                    *(volatile unsigned int *)(sfetch + 1) = g2 < nchunks ? g2 : kFetchDone;
+                }
             }
             g = __shfl_sync(kFull, g, 0);
-            if (g >= nchunks) break;
-            cid = (uint32_t)g;
+            if (g == kFetchDone) break;
+            cid = g;
             sidx = 0;
         }
-        const uint32_t sg = cid * kPullChunkSubs + sidx;
-        if (sg >= nsub) continue;
-        {
-            const uint32_t wbase = w0 + sg * kPullSub;
-            const uint32_t myw = wbase + lane;
-            const bool mine = lane < (unsigned)kPullSub && myw < wend;
-            uint32_t vis = 0xffffffffu, cand = 0;
-            if (mine) {
-                vis = c.visited[myw];
-                cand = ~(vis | __ldg(noin + myw));   // padding bits are set in noin
-                if (!cand) fbm_next[myw] = 0u;
-                wfound[lane] = 0u;
-            }
-            // compact the candidates of the sub-tile into wbuf (vertex order)
-            const uint32_t cnt = __popc(cand);
-            uint32_t incl = cnt;
+        const uint32_t ug = cid * kPullChunkSubs + sidx;
+        if (ug >= nunit) continue;
+        const uint32_t ubase = w0 + ug * (G * kPullSub);
+        const uint32_t myw = ubase + lane;
+        const bool mine = lane < (unsigned)(G * kPullSub) && myw < wend;
+        uint32_t vis = 0xffffffffu, cand = 0;
+        if (mine) {
+            vis = c.visited[myw];
+            cand = ~(vis | __ldg(noin + myw));   // padding bits are set in noin
+            if (!cand) fbm_next[myw] = 0u;
+        }
+        if (G > 1 && !__any_sync(kFull, cand != 0u)) continue;
+        // candidate counts, scanned within each sub-tile's kPullSub lanes
+        const uint32_t cnt = __popc(cand);
+        uint32_t incl = cnt;
 #pragma unroll
-            for (int o = 1; o < kPullSub; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(kFull, incl, o);
-                if (lane >= (unsigned)o) incl += t;
-            }
-            const uint32_t total = __shfl_sync(kFull, incl, kPullSub - 1);
+        for (int o = 1; o < kPullSub; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o, kPullSub);
+            if ((lane & (kPullSub - 1)) >= (unsigned)o) incl += t;
+        }
+#pragma unroll 1
+        for (int s = 0; s < G; ++s) {
+            const uint32_t total = __shfl_sync(kFull, incl, s * kPullSub + kPullSub - 1);
             if (!total) continue;
+            const uint32_t wbase = ubase + s * kPullSub;
+            if (lane < (unsigned)kPullSub) wfound[lane] = 0u;
             {
-                // all 32 lanes scatter one word at a time (lane l places bit
-                // l of word w): no serial per-bit loop on 8 divergent lanes
+                // compact the candidates of the sub-tile into wbuf (vertex
+                // order): all 32 lanes scatter one word at a time (lane l
+                // places bit l of word w), no serial per-bit loop
                 const uint32_t excl = incl - cnt;
                 const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
                 for (int w = 0; w < kPullSub; ++w) {
-                    const uint32_t cw = __shfl_sync(kFull, cand, w);
-                    const uint32_t ow = __shfl_sync(kFull, excl, w);
+                    const uint32_t cw = __shfl_sync(kFull, cand, s * kPullSub + w);
+                    const uint32_t ow = __shfl_sync(kFull, excl, s * kPullSub + w);
                     if ((cw >> lane) & 1u) wbuf[ow + __popc(cw & lt)] = (wbase + w) * 32 + lane;
                 }
             }
@@ -1203,8 +1245,8 @@ __device__ __forceinline__ void pull_body(const LevelCtx &c, unsigned int *sn,
             }
             em.tile();
             __syncwarp();
-            if (mine && cand) {
-                const uint32_t fm = wfound[lane];
+            if (mine && cand && (lane / kPullSub) == (unsigned)s) {
+                const uint32_t fm = wfound[lane & (kPullSub - 1)];
                 fbm_next[myw] = fm;
                 if (fm) c.visited[myw] = vis | fm;
             }
@@ -1232,11 +1274,11 @@ k_pull(LevelCtx c, const uint32_t *__restrict__ in_off, const uint32_t *__restri
        uint32_t *__restrict__ fbm_next, uint64_t word0, uint64_t words) {
     __shared__ unsigned int sn;
     __shared__ SmemPull sp;
-    __shared__ unsigned int sfetch;
+    __shared__ unsigned int sfetch[2];
     zero_slot(c);
     const unsigned w = threadIdx.x >> 5;
     pull_body<VAR>(c, &sn, in_off, src, first_src, noin, fbm_next, word0, words, sp.list[w],
-                   sp.found[w], &sfetch);
+                   sp.found[w], sfetch);
 }
 
 // CTA-centric pull for in-degree > kPullHeavy: each CTA scans one kUnit
@@ -1431,6 +1473,17 @@ static __global__ void k_noin(const uint32_t *__restrict__ in_off, uint64_t n, u
 }
 
 // Largest out-degree (decides the megakernel's solo mode).
+static __global__ void __launch_bounds__(kBlock)
+k_count_bits(const uint32_t *__restrict__ bm, uint64_t words, unsigned long long *out) {
+    unsigned long long c = 0;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x)
+        c += __popc(bm[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 static __global__ void k_max_degree(const uint32_t *__restrict__ out_off, uint64_t n,
                                     unsigned int *out) {
     unsigned int mx = 0;

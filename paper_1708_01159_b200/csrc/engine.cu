@@ -78,16 +78,18 @@ struct abfs_traversal {
     uint32_t *hroots = nullptr, *droots = nullptr;            // batch roots (pinned / device)
     unsigned long long *dsums = nullptr;                     // per-root depth checksums (device)
     uint32_t *acc = nullptr;                                 // RED-mode candidate bits [words], all-zero between levels
+    uint32_t *pl = nullptr;                                  // list-based pull: 3 x [n] candidate lists
     std::vector<unsigned char> last_blob;                    // tree blob resident on the device
     std::vector<unsigned long long> batch_levels;            // per-root level counts, last launch
     size_t batch_recs = 0;                                   // records kept in mrecs, last launch
     unsigned char *dtree = nullptr, *htree = nullptr;   // device / pinned staging blob
     size_t tree_cap = 0;
     uint64_t max_out_degree = 0;   // decides the megakernel's cluster solo mode
+    uint64_t n_noin = 0;           // vertices of in-degree 0 (sparse-pull estimate)
     int mega_grid = 0;
     int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
     SoloState *dsolo = nullptr; // solo-mode hand-off (device)
-    int mega_minb = 5;          // resident CTAs per SM the megakernel is compiled for
+    int mega_minb = kMegaMinB;  // resident CTAs per SM the megakernel is compiled for
     char *stage = nullptr;                     // pinned D2H staging (2 chunks)
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
@@ -341,6 +343,17 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
             }
             cudaFree(dmax);
         }
+        if (e == cudaSuccess) {
+            unsigned long long *dcnt = nullptr, hc = 0;
+            e = cudaMalloc(&dcnt, sizeof(unsigned long long));
+            if (e == cudaSuccess) e = cudaMemset(dcnt, 0, sizeof(unsigned long long));
+            if (e == cudaSuccess) {
+                k_count_bits<<<grid_for(t->words, kBlock, 148 * 16), kBlock>>>(t->noin, t->words, dcnt);
+                e = cudaMemcpy(&hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost);
+            }
+            cudaFree(dcnt);
+            t->n_noin = hc - (t->words * 32 - n);   // padding bits are set
+        }
     }
     if (e != cudaSuccess) {
         set_error(std::string("traversal_create: ") + cudaGetErrorString(e));
@@ -373,6 +386,7 @@ extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     cudaFree(t->droots);
     cudaFree(t->dsums);
     cudaFree(t->acc);
+    cudaFree(t->pl);
     cudaFree(t->dtree);
     if (t->htree) cudaFreeHost(t->htree);
     if (t->stage) cudaFreeHost(t->stage);
@@ -600,7 +614,7 @@ int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device) {
     static int grids[64] = {0};
     if (device < 0 || device >= 64) return fail(ABFS_EINVAL, "device ordinal out of range");
     int &grid = grids[device];
-    void *kfn = (void *)k_mega<5>;
+    void *kfn = (void *)k_mega<kMegaMinB>;
     if (!grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -634,9 +648,13 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaMalloc((void **)&t->dsums, kMaxBatch * sizeof(unsigned long long)));
     }
     if (nroots < 1 || nroots > kMaxBatch) return fail(ABFS_EINVAL, "bad root count");
+#ifdef ABFS_MEGA_VARIANTS   // occupancy experiments (set_mode 2 / 3)
     void *kfn = t->mega_minb == 4   ? (void *)k_mega<4>
-                : t->mega_minb == 5 ? (void *)k_mega<5>
-                                    : (void *)k_mega<6>;
+                : t->mega_minb == 6 ? (void *)k_mega<6>
+                                    : (void *)k_mega<kMegaMinB>;
+#else
+    void *kfn = (void *)k_mega<kMegaMinB>;
+#endif
     if (!t->mega_grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -698,7 +716,8 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     if (host_init) {
         ABFS_TRY(init_impl(t, roots[0]));
         ABFS_CUDA(cudaMemsetAsync(t->dctr, 0, offsetof(Ctr, cq), s));
-        ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(unsigned) * 4 + 8 * 3 + 8 * 3, s));
+        // every megakernel slot array from cq3 on (cq3, es3, work, ps, pc)
+        ABFS_CUDA(cudaMemsetAsync(&t->dctr->cq3[0], 0, sizeof(Ctr) - offsetof(Ctr, cq3), s));
     } else {
         std::memcpy(t->hroots, roots, nroots * sizeof(uint32_t));
         ABFS_CUDA(cudaMemcpyAsync(t->droots, t->hroots, nroots * sizeof(uint32_t),
@@ -773,6 +792,21 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.acc = nullptr;
     P.red_frontier = env_u64("ABFS_RED_F", g.n >> 7 > 4096 ? g.n >> 7 : 4096);
     P.red_units = (uint32_t)env_u64("ABFS_RED_UNITS", 0xffffffffull);
+    P.n_noin = t->n_noin;
+    // list-based pull levels (pull2.cuh), opt-in with ABFS_PULL2=1: measured
+    // slower than the sub-tile pull on B200 (K24 8 roots: 2967 vs 2233 us;
+    // the grid-wide probe-0 sweep moves no more loads per warp round trip
+    // than the sub-tile chain, and the survivors' scans lose the L1 reuse of
+    // the offsets their probe just loaded), kept tested for the carried-list
+    // tail levels it does speed up
+    P.pl_s = P.pl_c0 = P.pl_c1 = nullptr;
+    if (env_u64("ABFS_PULL2", 0) && g.n < (1ull << 31)) {
+        if (!t->pl) ABFS_CUDA(cudaMalloc((void **)&t->pl, 3 * (g.n + 4) * sizeof(uint32_t)));
+        P.pl_s = t->pl;
+        P.pl_c0 = t->pl + (g.n + 4);
+        P.pl_c1 = t->pl + 2 * (g.n + 4);
+    }
+    P.pull_wide_max = env_u64("ABFS_PULL_WIDE", g.n >> 5);
     if (env_u64("ABFS_RED", 1)) {
         if (!t->acc) {
             ABFS_CUDA(cudaMalloc((void **)&t->acc, (t->words + 4) * 4));
@@ -860,7 +894,7 @@ extern "C" int abfs_traversal_set_mode(abfs_traversal *t, int device_loop) {
     if (!t) return fail(ABFS_EINVAL, "null traversal");
     ABFS_LOCK(t);
     t->use_mega = device_loop != 0;
-    const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 6 : 5;
+    const int minb = device_loop == 3 ? 4 : device_loop == 2 ? 6 : kMegaMinB;
     if (minb != t->mega_minb) {
         t->mega_minb = minb;
         t->mega_grid = 0;

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "bfs_kernels.cuh"
+#include "pull2.cuh"
 
 namespace abfs {
 
@@ -94,6 +95,14 @@ struct MegaParams {
     uint32_t *acc;
     uint64_t red_frontier;
     uint32_t red_units;
+    // sparse pull levels: when at most pull_wide_max candidates can remain
+    // (|V| - discovered - n_noin, n_noin = vertices of in-degree 0) the pull
+    // sweeps 4 sub-tiles per warp fetch (0 disables)
+    uint64_t pull_wide_max;
+    uint64_t n_noin;
+    // list-based pull (pull2.cuh; single graph): survivor list + two
+    // carried candidate lists, each [n] (pl_s = nullptr: sub-tile pull)
+    uint32_t *pl_s, *pl_c0, *pl_c1;
 };
 
 // Order-sensitive checksum term of one vertex's depth (numpy restatement in
@@ -212,7 +221,8 @@ __device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx
                                              uint32_t F, const uint32_t *q, uint32_t *fbm_next,
                                              SmemQ *sq, unsigned *sn, int *s_done,
                                              uint32_t *pfound, unsigned int *sfetch,
-                                             unsigned *warp_tot, unsigned *s_base,
+                                             unsigned *warp_tot, unsigned *s_base, bool wide,
+                                             const PullLists *PL, uint32_t pl_n,
                                              cg::grid_group &grid) {
     // Two-phase strategies (light pass, then CTA work units) need a second
     // barrier only if the light pass created units: after the first barrier
@@ -248,12 +258,42 @@ __device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx
         return c.acc ? kStratBitmap : 0;
     }
     case 3:
+        if (PL) {
+            // list-based pull: probe 0 grid-wide, then the survivors' scans
+            CEmit<VAR> em(sn, c.count);
+            unsigned long long scanned = 0;
+            if (PL->c_in)
+                pull2_list_probe(c, PL->c_in, pl_n, P.first_src, fbm_next, P.wlo, P.wend, scanned);
+            else
+                pull2_sweep<VAR>(c, em, P.noin, P.first_src, fbm_next, P.wlo, P.wend, *PL, warp_tot,
+                                 s_base, scanned);
+            ABFS_DIAG_MARK(1);   // diagnostic builds: phase-1 end in the unit-pass slot
+            grid.sync();
+            const uint32_t *lst = PL->c_in ? PL->c_in : PL->s;
+            const uint32_t nl = PL->c_in ? pl_n : *(volatile unsigned *)PL->s_tail;
+            pull2_scan<VAR>(c, em, lst, nl, P.in_off, P.src, fbm_next, *PL, warp_tot, s_base, scanned);
+            em.finish();
+            ABFS_DIAG_MARK(0);
+            if (c.es) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) scanned += __shfl_down_sync(kFull, scanned, o);
+                if ((threadIdx.x & 31) == 0 && scanned) atomicAdd(c.es, scanned);
+            }
+            grid.sync();
+            if (!units()) return 0;
+            pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
+            break;
+        }
         {
             // the pull scratch lists alias the (idle) CTA queue buffer
             static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");
             const unsigned w = threadIdx.x >> 5;
-            pull_body<VAR>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, P.wlo, P.wend,
-                           sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
+            if (wide)
+                pull_body<VAR, 4>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, P.wlo,
+                                  P.wend, sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
+            else
+                pull_body<VAR, 1>(c, sn, P.in_off, P.src, P.first_src, P.noin, fbm_next, P.wlo,
+                                  P.wend, sq->buf + w * kPullList, pfound + w * kPullSub, sfetch);
         }
         ABFS_DIAG_MARK(0);
         grid.sync();
@@ -283,13 +323,18 @@ __device__ __forceinline__ bool solo_fits(const MegaParams &P, int kernel,
     return false;
 }
 
+#ifndef ABFS_MEGA_MINB
+#define ABFS_MEGA_MINB 5
+#endif
+constexpr int kMegaMinB = ABFS_MEGA_MINB;   // default variant (set_mode 1)
+
 // MINB = resident CTAs per SM the register budget is sized for (6 -> 40
 // registers, 4 -> 64); latency-bound pull levels want the higher occupancy.
 template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
     __shared__ uint32_t pfound[kWarps * kPullSub];
-    __shared__ unsigned int s_fetch;
+    __shared__ unsigned int s_fetch[2];
     __shared__ unsigned sn;
     __shared__ int s_done;
     __shared__ int s_cls;
@@ -344,6 +389,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                 P.ctr->cq3[s] = 0;
                 P.ctr->es3[s] = 0;
                 P.ctr->work[s] = 0;
+                P.ctr->ps[s] = 0;
+                P.ctr->pc[s] = 0;
             }
             P.ctr->cq = 0;
             P.ctr->inconsistent = 0;
@@ -354,6 +401,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
     int cur = 0;
     bool has_q = true, has_bm = true;
+    int pl_have = -1;      // carried pull candidate list: -1 none, 0 / 1 = pl_c0 / pl_c1
+    uint32_t pl_n = 0;
     uint32_t solo_skip = 0xffffffffu;
     for (uint32_t level = 0;; ++level) {
         const unsigned long long t0 = lead ? globaltimer() : 0ull;
@@ -375,6 +424,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             P.ctr->cq3[zero] = 0;
             P.ctr->es3[zero] = 0;
             P.ctr->work[zero] = 0;
+            P.ctr->ps[zero] = 0;
+            P.ctr->pc[zero] = 0;
         }
         if (P.solo_ctas && has_q && level != solo_skip && solo_fits(P, pk, frontier)) {
             // ---- cluster solo mode: cluster 0 runs this level and the
@@ -522,6 +573,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                 has_q = st->has_q != 0;
                 has_bm = st->has_bm != 0;
                 solo_skip = L;   // the grid runs level L (never solo again)
+                pl_have = -1;    // solo levels are top-down
                 level = L - 1;   // ++level
             }
             grid.sync();         // everyone has read the hand-off before it is reused
@@ -573,13 +625,32 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
         uint32_t *pull_next = P.part ? P.fnext : fbm_nxt;
+        // list-based pull (single graph): sweep after a top-down level, the
+        // carried candidate list after a pull level
+        PullLists pl;
+        const bool use_pl = pk == 3 && P.pl_s && !P.part;
+        if (use_pl) {
+            pl.s = P.pl_s;
+            pl.c_in = pl_have >= 0 ? (pl_have ? P.pl_c1 : P.pl_c0) : nullptr;
+            pl.c_out = pl_have == 0 ? P.pl_c1 : P.pl_c0;
+            pl.s_tail = &P.ctr->ps[out];
+            pl.c_tail = &P.ctr->pc[out];
+        }
+        const unsigned long long settled = discovered + P.n_noin;
+        const bool wide = P.pull_wide_max && (settled >= P.n || P.n - settled <= P.pull_wide_max);
         int sflags;
         switch (pv) {
-        case 0: sflags = mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
-        case 1: sflags = mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
-        default: sflags = mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, &s_fetch, warp_tot, &s_base, grid); break;
+        case 0: sflags = mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, s_fetch, warp_tot, &s_base, wide, use_pl ? &pl : nullptr, pl_n, grid); break;
+        case 1: sflags = mega_strategy<1>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, s_fetch, warp_tot, &s_base, wide, use_pl ? &pl : nullptr, pl_n, grid); break;
+        default: sflags = mega_strategy<2>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, s_fetch, warp_tot, &s_base, wide, use_pl ? &pl : nullptr, pl_n, grid); break;
         }
         const bool topdown = pk != 3;
+        if (use_pl) {   // the candidates this pull leaves for the next one
+            pl_have = pl_have == 0 ? 1 : 0;
+            pl_n = *(volatile unsigned *)&P.ctr->pc[out];
+        } else {
+            pl_have = -1;
+        }
         unsigned long long nw;
         if (P.part) {
             // fused frontier exchange: the visited bits this rank gained are

@@ -504,3 +504,26 @@ def test_red_mode_batch_checksums_k18(red_mode):
         hist = np.bincount(want[want != G.INF], minlength=n)
         assert per[i] == hist[1:n].tolist() + [0], r
     t.close()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_list_pull_all_pairs_and_traces_match_reference(name, monkeypatch):
+    """The megakernel's list-based pull (pull2.cuh, ABFS_PULL2=1: grid-wide
+    probe-0 sweep or carried candidate list, then the survivors' scans)
+    reproduces every golden depth array, count and trace."""
+    monkeypatch.setenv("ABFS_PULL2", "1")
+    g = graph(name)
+    stats = P.compute_stats(g)
+    traces = G.traces()["small"]
+    for r in G.roots(name):
+        want = G.depth(name, r)
+        for v in P.CountVariant:
+            d, outs = P.bfs_full(g, r, P.KernelId.VERTEX_PULL, v)
+            np.testing.assert_array_equal(d, want, err_msg=f"{name} root={r} {v.name}")
+            assert [o.new_frontier_count for o in outs] == G.counts(name, r).tolist()
+        for key, tree in G.trees_for(name):
+            d, tr = P.adaptive_bfs(g, r, P.deserialize(G.tree_path(tree)), stats)
+            got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                   for x in tr.records]
+            assert got == traces[name][str(r)][key], (name, r, key)
+            np.testing.assert_array_equal(d, want)

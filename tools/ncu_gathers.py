@@ -14,7 +14,7 @@ import re
 import subprocess
 import tempfile
 
-OWN = ("bfs_kernels.cuh", "megakernel.cuh", "engine.cu", "partition.cu", "launch.cuh")
+OWN = ("bfs_kernels.cuh", "megakernel.cuh", "pull2.cuh", "engine.cu", "partition.cu", "launch.cuh")
 
 
 def line_map(cubin, kern):
