@@ -190,7 +190,6 @@ def test_enumerations():
     for i, (k, v) in enumerate(P.ALL_PAIRS):
         assert P.pair_index(k, v) == i and P.pair_from_index(i) == (k, v)
     assert P.INF_DEPTH == 2**31 - 1
-    assert P.bucket_for(1.05) == "optimal" and P.bucket_for(2.5) is None
     with pytest.raises(ValueError):
         P.set_worker_count(0)
 
