@@ -82,6 +82,11 @@ typedef struct {
     uint64_t new_count;
     uint64_t elapsed_ns;      /* CUDA-event time of the level incl. conversion */
     uint64_t prediction_ns;   /* host feature extraction + tree descent        */
+    /* SURVEY §8a N2, per-level integer features from the device: */
+    uint64_t unvisited;       /* |V| - discovered after this level (exact)           */
+    uint64_t next_out_edges;  /* sum of out-degrees of this level's discoveries (the
+                                 next frontier's out-edges); measured in instrumented
+                                 runs (abfs_traversal_instrument), else UINT64_MAX */
 } abfs_level_record;
 
 ABFS_API const char *abfs_last_error(void);

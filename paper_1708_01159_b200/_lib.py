@@ -48,7 +48,8 @@ class AbfsLevelRecord(ctypes.Structure):
                 ("variant", ctypes.c_int32), ("fallback", ctypes.c_int32),
                 ("converted", ctypes.c_int32), ("frontier_size", ctypes.c_uint64),
                 ("new_count", ctypes.c_uint64), ("elapsed_ns", ctypes.c_uint64),
-                ("prediction_ns", ctypes.c_uint64)]
+                ("prediction_ns", ctypes.c_uint64), ("unvisited", ctypes.c_uint64),
+                ("next_out_edges", ctypes.c_uint64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/abfs.h.

@@ -63,6 +63,7 @@ struct Ctr {
     unsigned long long work[3];  // per-level dynamic work cursors
     unsigned int ps[3];          // megakernel pull: survivor-list tails
     unsigned int pc[3];          // megakernel pull: carried-candidate-list tails
+    unsigned long long oe3[3];   // megakernel: N2 next-frontier out-edges (instrumented)
 };
 
 // Host-mapped result of the last level (written by the device).

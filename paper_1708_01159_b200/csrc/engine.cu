@@ -1026,10 +1026,14 @@ extern "C" int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tre
         if (recs && nl > t->hrecs.size() && cap > t->hrecs.size())
             goto launch_path;   // > kMegaCap levels: the launch path records them all
         *n_levels = nl;
+        uint64_t disc = 1;
         if (recs)
             for (size_t l = 0; l < nl && l < cap && l < t->hrecs.size(); ++l) {
                 const MegaRecord &m = t->hrecs[l];
                 abfs_level_record &r = recs[l];
+                disc += m.new_count;
+                r.unvisited = t->g->d.n - disc;
+                r.next_out_edges = t->instrument ? m.next_out_edges : ~0ull;
                 r.level = (int64_t)l;
                 r.kernel = m.kernel;
                 r.variant = m.variant;
@@ -1074,6 +1078,8 @@ launch_path:
             r.new_count = c;
             r.elapsed_ns = 0;   // filled from the level's events after the traversal
             r.prediction_ns = pred ? pred : 1;
+            r.unvisited = t->g->d.n - (discovered + c);
+            r.next_out_edges = ~0ull;   // instrumented runs: filled below
         }
         if (c == 0) {
             *n_levels = (size_t)level + 1;
@@ -1085,6 +1091,15 @@ launch_path:
     ABFS_TRY(finish_traversal(t, *n_levels, depths_out));
     if (recs)
         for (size_t l = 0; l < *n_levels && l < cap; ++l) ABFS_TRY(event_ns(t, l, &recs[l].elapsed_ns));
+    if (recs && t->instrument) {
+        // launch path: the discoveries of level l are the depth-(l+1)
+        // vertices; one device histogram of the final depths gives every
+        // level's next-frontier out-edges
+        const size_t nl = *n_levels;
+        std::vector<uint64_t> cnt(nl + 2), od(nl + 2), idg(nl + 2);
+        ABFS_TRY(abfs_traversal_level_stats(t, nl + 1, cnt.data(), od.data(), idg.data(), nullptr));
+        for (size_t l = 0; l < nl && l < cap; ++l) recs[l].next_out_edges = od[l + 1];
+    }
     return ABFS_OK;
 }
 

@@ -30,6 +30,7 @@ struct MegaRecord {
     unsigned long long frontier, new_count;
     unsigned long long t_start, t_pred, t_end;   // %globaltimer (ns)
     unsigned long long scanned;                  // pull ES (instrumented)
+    unsigned long long next_out_edges;           // N2: sum out-degree of the discoveries (instrumented)
 };
 
 struct MegaParams {
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                 P.ctr->work[s] = 0;
                 P.ctr->ps[s] = 0;
                 P.ctr->pc[s] = 0;
+                P.ctr->oe3[s] = 0;
             }
             P.ctr->cq = 0;
             P.ctr->inconsistent = 0;
@@ -426,8 +428,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             P.ctr->work[zero] = 0;
             P.ctr->ps[zero] = 0;
             P.ctr->pc[zero] = 0;
+            P.ctr->oe3[zero] = 0;
         }
-        if (P.solo_ctas && has_q && level != solo_skip && solo_fits(P, pk, frontier)) {
+        // (instrumented work-model runs take the grid path: it records N2 features)
+        if (P.solo_ctas && !P.instrument && has_q && level != solo_skip && solo_fits(P, pk, frontier)) {
             // ---- cluster solo mode: cluster 0 runs this level and the
             // following small top-down levels alone (cluster barriers,
             // ~0.3 us) while every other CTA waits at ONE grid barrier
@@ -704,6 +708,34 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             nw = topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
                          : *(volatile unsigned long long *)&P.ctr->count[out];
         }
+        // N2 (instrumented runs only): sum of the out-degrees of this level's
+        // discoveries -- the next frontier's out-edges -- reduced on the device
+        unsigned long long next_oe = ~0ull;
+        if (P.instrument && !P.part) {
+            const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+            const uint64_t nt = (uint64_t)gridDim.x * kBlock;
+            unsigned long long acc = 0;
+            if (topdown) {
+                for (uint64_t i = tid; i < nw; i += nt) {
+                    const uint32_t v = q_nxt[i];
+                    acc += P.out_off[v + 1] - P.out_off[v];
+                }
+            } else {
+                for (uint64_t w = tid; w < P.words; w += nt) {
+                    uint32_t x = pull_next[w];
+                    while (x) {
+                        const uint64_t v = w * 32 + (__ffs(x) - 1);
+                        acc += P.out_off[v + 1] - P.out_off[v];
+                        x &= x - 1;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+            if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&P.ctr->oe3[out], acc);
+            grid.sync();
+            next_oe = *(volatile unsigned long long *)&P.ctr->oe3[out];
+        }
 #ifdef ABFS_NO_RECORDS   // overhead experiment only
         if (false) {
 #else
@@ -720,6 +752,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.t_pred = tp;
             r.t_end = globaltimer();
             // partitions: this rank's count through the level's count variant
+            r.next_out_edges = next_oe;
             r.scanned = P.part ? (topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
                                           : *(volatile unsigned long long *)&P.ctr->count[out])
                       : P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;

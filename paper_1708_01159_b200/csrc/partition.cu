@@ -876,6 +876,8 @@ static int parts_traverse(abfs_part *const *parts, uint32_t nparts, int64_t root
             r.new_count = g;
             r.elapsed_ns = ns;
             r.prediction_ns = 1;
+            r.unvisited = parts[0]->n - (discovered + g);
+            r.next_out_edges = ~0ull;
         }
         if (g == 0) {
             *n_levels = (size_t)level + 1;
@@ -1022,9 +1024,13 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
         return parts_traverse(one, 1, root, tr, static24, fixed_pair, chunk, recs, local_counts,
                               cap, n_levels);
     }
+    uint64_t disc = 1;
     for (size_t l = 0; recs && l < keep && l < cap; ++l) {
         const MegaRecord &m = p->mrecs[l];
         abfs_level_record &r = recs[l];
+        disc += m.new_count;
+        r.unvisited = p->n - disc;
+        r.next_out_edges = ~0ull;
         r.level = (int64_t)l;
         r.kernel = m.kernel;
         r.variant = m.variant;

@@ -183,3 +183,40 @@ def test_reached_edges_and_level_hist(name):
     finally:
         t.close()
         dg.close()
+
+
+@pytest.mark.parametrize("name", ["kron12", "er12", "mesh64", "u1000", "unreach"])
+def test_per_level_device_features(name):
+    """every level record carries unvisited = |V| - discovered
+    (exact, always) and, in instrumented runs, the sum of out-degrees of the
+    level's discoveries (the next frontier's out-edges) reduced on the device
+    -- both level drivers, checked against the golden depths."""
+    n, m, a = G.graph_arrays(name)
+    g = P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS])
+    dg = DeviceGraph.upload(g)
+    t = Traversal(dg)
+    od = np.diff(a["out_offsets"].astype(np.int64))
+    flat = P.deserialize(G.tree_path("t1"))
+    st = static_vector(P.compute_stats(g))
+    try:
+        for r in G.roots(name):
+            want = G.depth(name, r)
+            reach = want != INF
+            for loop in (True, False):
+                t.set_device_loop(loop)
+                for inst in (False, True):
+                    t.instrument(inst)
+                    recs = t.adaptive(r, flat.as_abfs(), st, 32)
+                    for x in recs:
+                        L = x.level
+                        assert x.unvisited == n - int((reach & (want <= L + 1)).sum()), (name, r, L)
+                        if inst:
+                            assert x.next_out_edges == int(od[reach & (want == L + 1)].sum()), \
+                                (name, r, loop, L)
+                        else:
+                            assert x.next_out_edges == 2**64 - 1
+            t.set_device_loop(True)
+            t.instrument(False)
+    finally:
+        t.close()
+        dg.close()

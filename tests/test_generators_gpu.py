@@ -64,3 +64,46 @@ def test_device_build_combined_and_upload(name):
     got = up.download(rev_owner=True)
     for k in G.ARRAYS + ("rev_owner",):
         np.testing.assert_array_equal(got[k], a[k], err_msg=k)
+
+
+def test_reference_named_construction_routes_to_the_device(monkeypatch):
+    """build_combined / generate_graph (graph.py:93-134, 211-252) build large
+    inputs in HBM: the arrays equal the host construction's, stats are taken
+    from the offsets only, and traversals use the resident copy (no upload)."""
+    from paper_1708_01159_b200.graph import DeviceResidentGraph
+    rng = np.random.default_rng(5)
+    n = 5000
+    pairs = rng.integers(0, n, size=(40000, 2))
+    host = P.build_combined(pairs, n)
+    monkeypatch.setenv("ABFS_DEVICE_BUILD_MIN_EDGES", "1000")
+    dev = P.build_combined(pairs, n)
+    assert isinstance(dev, DeviceResidentGraph) and not isinstance(host, DeviceResidentGraph)
+    st = P.compute_stats(dev)
+    assert dev._host is None          # stats did not download the edge arrays
+    assert st == P.compute_stats(host)
+    for k in ("out_offsets", "destinations", "origins", "in_offsets", "sources"):
+        np.testing.assert_array_equal(getattr(dev, k), getattr(host, k), err_msg=k)
+    np.testing.assert_array_equal(dev.rev_owner(), host.rev_owner())
+    for r in (0, 17, 4999):
+        d1, _ = P.bfs_full(dev, r, P.KernelId.VERTEX_PULL, P.CountVariant.GROUP_REDUCE)
+        np.testing.assert_array_equal(d1, P.reference_bfs(host, r))
+    assert dev.device_graph() is dev._dg
+    # generators: rmat-like and uniform-random straight on the device
+    for model, params in (("rmat-like", {"scale": 12, "edges": 16 << 12}),
+                          ("uniform-random", {"n": 1 << 12, "edges": 20 << 12})):
+        g_dev = P.generate_graph(model, params, 3)
+        assert isinstance(g_dev, DeviceResidentGraph)
+        monkeypatch.setenv("ABFS_DEVICE_BUILD_MIN_EDGES", str(1 << 40))
+        g_host = P.generate_graph(model, params, 3)
+        monkeypatch.setenv("ABFS_DEVICE_BUILD_MIN_EDGES", "1000")
+        assert not isinstance(g_host, DeviceResidentGraph)
+        for k in ("out_offsets", "destinations", "origins", "in_offsets", "sources"):
+            np.testing.assert_array_equal(getattr(g_dev, k), getattr(g_host, k), err_msg=(model, k))
+    # non-power-of-two uniform: host draws (the device stream needs 2^k), then
+    # the device build of the pairs -- still the reference's arrays
+    g = P.generate_graph("uniform-random", {"n": 3000, "edges": 5000}, 1)
+    monkeypatch.setenv("ABFS_DEVICE_BUILD_MIN_EDGES", str(1 << 40))
+    h = P.generate_graph("uniform-random", {"n": 3000, "edges": 5000}, 1)
+    assert isinstance(g, DeviceResidentGraph) and not isinstance(h, DeviceResidentGraph)
+    for k in ("out_offsets", "destinations", "origins", "in_offsets", "sources"):
+        np.testing.assert_array_equal(getattr(g, k), getattr(h, k), err_msg=k)
