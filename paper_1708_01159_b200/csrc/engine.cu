@@ -124,6 +124,16 @@ static uint64_t env_u64(const char *name, uint64_t dflt) {
     return (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : dflt;
 }
 
+// Push-warp's virtual-warp width: the reference's chunk size is a schedule
+// parameter (depths and counts do not depend on it, kernels.py:303-322), so
+// a graph whose out-degrees are all below the chunk gets warps no wider than
+// its largest adjacency (mesh: 4 lanes per vertex instead of 32, 28 idle).
+static int64_t vw_chunk(const abfs_traversal *t, int64_t chunk) {
+    int64_t w = 1;
+    while (w < (int64_t)t->max_out_degree && w < 32) w <<= 1;
+    return chunk < w ? chunk : w;
+}
+
 // One level's strategy launch over a StratArgs view (launch.cuh).
 template <int VAR>
 static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, int64_t chunk) {
@@ -144,7 +154,7 @@ static void launch_strategy(abfs_traversal *t, const LevelCtx &c, int kernel, in
     a.word_end = t->words;
     a.q = t->q[t->cur];
     a.F = (uint32_t)t->F;
-    t->launches += launch_strategy_args<VAR>(c, a, kernel, chunk, t->stream);
+    t->launches += launch_strategy_args<VAR>(c, a, kernel, vw_chunk(t, chunk), t->stream);
 }
 
 static int ensure_events(abfs_traversal *t, size_t n) {
@@ -747,7 +757,10 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.tree = t->dtree;
     P.tree_nodes = nn;
     P.fixed_pair = fixed_pair;
-    P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
+    {
+        const int64_t vc = vw_chunk(t, chunk);
+        P.vw_log2 = vc >= 32 ? 5 : vc >= 16 ? 4 : vc >= 8 ? 3 : vc >= 4 ? 2 : vc >= 2 ? 1 : 0;
+    }
     P.instrument = t->instrument ? 1 : 0;
     P.pull_light = pull_light();
     P.cap = kMegaCap;
