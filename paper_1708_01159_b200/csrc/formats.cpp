@@ -263,6 +263,7 @@ extern "C" int abfs_trace_read(const char *path, abfs_level_record *recs, size_t
         }
         if (f.size() != 7) return fail(ABFS_EINVAL, "malformed trace row " + std::to_string(i));
         abfs_level_record r{};
+        r.next_out_edges = ~0ull;   // not a trace-CSV column (unvisited: 0 = not recorded)
         r.level = std::strtoll(f[0].c_str(), nullptr, 10);
         r.kernel = r.variant = -1;
         for (int q = 0; q < 5; ++q)
