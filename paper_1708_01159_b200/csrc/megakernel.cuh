@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                         P.ctr->cq3[z] = 0;
                         P.ctr->es3[z] = 0;
                         P.ctr->work[z] = 0;
+                        P.ctr->ps[z] = 0;
+                        P.ctr->pc[z] = 0;
+                        P.ctr->oe3[z] = 0;
                     }
                     LevelCtx sc;
                     sc.acc = nullptr;
