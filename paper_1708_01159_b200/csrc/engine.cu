@@ -124,13 +124,24 @@ static uint64_t env_u64(const char *name, uint64_t dflt) {
     return (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : dflt;
 }
 
-// Push-warp's virtual-warp width: the reference's chunk size is a schedule
+// Push-warp's virtual-warp width.  The reference's chunk size is a schedule
 // parameter (depths and counts do not depend on it, kernels.py:303-322), so
-// a graph whose out-degrees are all below the chunk gets warps no wider than
-// its largest adjacency (mesh: 4 lanes per vertex instead of 32, 28 idle).
+// the width is fitted to the degree distribution: on a graph without a
+// heavy tail (max out-degree <= 4 x mean: uniform-random, meshes) a vertex's
+// adjacency is covered by 4 strides of mean/8 lanes (ER-32M: 4-lane warps,
+// its 18.6 M-discovery level 724 -> 617 us; mesh: 1 lane, as push); skewed
+// graphs keep warps of min(chunk, 32, max degree) lanes (Kronecker-24 is
+// 1-8 % slower with narrower warps).  ABFS_VW_MAX caps it for experiments.
 static int64_t vw_chunk(const abfs_traversal *t, int64_t chunk) {
+    const uint64_t n = t->g->d.n ? t->g->d.n : 1, mean = t->g->d.m / n;
     int64_t w = 1;
-    while (w < (int64_t)t->max_out_degree && w < 32) w <<= 1;
+    if (t->max_out_degree <= 4 * (mean ? mean : 1)) {
+        while (w * 2 <= (int64_t)(mean / 8) && w < 32) w <<= 1;
+    } else {
+        while (w < (int64_t)t->max_out_degree && w < 32) w <<= 1;
+    }
+    const int64_t cap = (int64_t)env_u64("ABFS_VW_MAX", 32);
+    if (w > cap) w = cap;
     return chunk < w ? chunk : w;
 }
 

@@ -320,7 +320,9 @@ __device__ __forceinline__ bool solo_fits(const MegaParams &P, int kernel,
     // one pass of the cluster's threads (two for virtual warps)
     const unsigned long long lanes = (unsigned long long)P.solo_ctas * kBlock;
     if (kernel == 2) return frontier <= lanes;
-    if (kernel == 4) return (frontier << P.vw_log2) <= 2 * lanes;
+    // virtual warps: two passes pay off for wide warps (few vertices per
+    // pass); narrow ones (a degree-fitted width of 1-2 lanes) are push-like
+    if (kernel == 4) return (frontier << P.vw_log2) <= (P.vw_log2 >= 2 ? 2 : 1) * lanes;
     return false;
 }
 
