@@ -171,8 +171,9 @@ def make_graph(a, dev):
                 "erdos-renyi-32M-deg32 (directed)")
     if a.graph == "mesh":      # config 4: 4096 x 4096 4-neighbour grid
         return DeviceGraph.mesh(4096, 4096, device=dev), True, "mesh-4096x4096"
-    return (DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev), True,
-            f"kronecker-{a.scale}-ef16-symmetrised")
+    return (DeviceGraph.rmat(a.scale, 16 << a.scale, 1, symmetrize=True, device=dev,
+                             permute=a.permute), True,
+            f"kronecker-{a.scale}-ef16-symmetrised" + ("-permuted-ids" if a.permute else ""))
 
 
 def run_ours(a):
@@ -388,7 +389,8 @@ def run_ours(a):
             "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator)",
+            "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator"
+                    + (", ids relabelled by a fixed bijection)" if a.permute else ")"),
             "config": {"workload": f"{wname} tree-switched BFS",
                        "graph": a.graph, "scale": a.scale, "vertices": V, "directed_edge_slots": E,
                        "teps_basis": "sum of out-degree of reached vertices" + (" / 2" if symmetric else ""),
@@ -875,6 +877,9 @@ def main():
                     help="--partition frontier exchange: fused peer stores or NCCL all-gather")
     ap.add_argument("--virtual-parts", type=int, default=8,
                     help="--partition at N=1: partitions sharing the one GPU")
+    ap.add_argument("--permute", action="store_true",
+                    help="Kronecker with ids relabelled by a fixed bijection (hubs spread over the "
+                         "id space; a robustness run, not the reference's generator)")
     ap.add_argument("--root-sharded", action="store_true",
                     help="N > 1: replicate the graph and shard the roots (no exchange) instead of "
                          "the 1-D partitioned BFS")

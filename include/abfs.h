@@ -108,7 +108,10 @@ ABFS_API int abfs_graph_build(int device, uint64_t n, uint64_t m, const uint32_t
 
 /* Device generators, bit-exact to generate_graph (graph.py:211-252):
  * pcg_state/pcg_inc are numpy default_rng(seed)'s PCG64 words (hi, lo).
- * symmetrize=1 appends the reversed pairs. */
+ * symmetrize bit 0 appends the reversed pairs; bit 1
+ * (rmat only, no reference counterpart) relabels ids with the bijection
+ * v -> (v * 0x9E3779B1 + 0x7F4A7C15) mod 2^scale, Graph500-style, so hubs are
+ * not clustered at low ids (robustness runs, bench.py --permute). */
 ABFS_API int abfs_graph_generate_rmat(int device, uint32_t scale, uint64_t edges,
                              double a, double b, double c,
                              const uint64_t pcg_state[2], const uint64_t pcg_inc[2],

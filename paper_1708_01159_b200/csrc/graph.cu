@@ -102,9 +102,18 @@ __global__ void k_gen_rmat(const RmatParams *__restrict__ P, uint64_t *keys_fwd)
     const int cnt = (int)min((uint64_t)kGenChunk, p.m - i0);
     uint32_t src[kGenChunk], dst[kGenChunk];
     rmat_pairs(p, i0, cnt, src, dst);
+    if (p.symmetrize & 2) {
+        // Graph500-style relabelling: an odd-multiplier affine map is a
+        // bijection of [0, 2^scale), so hubs no longer sit at low ids
+        const uint32_t mask = (uint32_t)((1ull << p.scale) - 1);
+        for (int k = 0; k < cnt; ++k) {
+            src[k] = (src[k] * 0x9E3779B1u + 0x7F4A7C15u) & mask;
+            dst[k] = (dst[k] * 0x9E3779B1u + 0x7F4A7C15u) & mask;
+        }
+    }
     for (int k = 0; k < cnt; ++k) {
         keys_fwd[i0 + k] = ((uint64_t)src[k] << 32) | dst[k];
-        if (p.symmetrize) keys_fwd[p.m + i0 + k] = ((uint64_t)dst[k] << 32) | src[k];
+        if (p.symmetrize & 1) keys_fwd[p.m + i0 + k] = ((uint64_t)dst[k] << 32) | src[k];
     }
 }
 
@@ -434,7 +443,7 @@ extern "C" int abfs_graph_generate_rmat(int device, uint32_t scale, uint64_t edg
     if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0 + 1e-9)
         return fail(ABFS_EINVAL, "rmat probabilities must be non-negative and sum to <= 1");
     const uint64_t n = 1ull << scale;
-    const uint64_t m = symmetrize ? 2 * edges : edges;
+    const uint64_t m = (symmetrize & 1) ? 2 * edges : edges;
     abfs_graph *g = nullptr;
     ABFS_TRY(new_graph(device, n, m, &g));
     RmatParams hp;
@@ -442,7 +451,7 @@ extern "C" int abfs_graph_generate_rmat(int device, uint32_t scale, uint64_t edg
     hp.inc = words_to_u128(pcg_inc);
     hp.m = edges;
     hp.scale = scale;
-    hp.symmetrize = symmetrize ? 1 : 0;
+    hp.symmetrize = symmetrize & 3;
     // Same float64 operations as graph.py:247-248: a+b and (a+b)+c.
     hp.t1 = thr53(a);
     hp.t2 = thr53(a + b);

@@ -60,14 +60,17 @@ class DeviceGraph:
 
     @classmethod
     def rmat(cls, scale: int, edges: int, seed: int, a=0.57, b=0.19, c=0.19,
-             symmetrize: bool = False, device: int = 0) -> "DeviceGraph":
+             symmetrize: bool = False, device: int = 0, permute: bool = False) -> "DeviceGraph":
         """generate_graph("rmat-like", ...) (graph.py:232-252) on the device,
-        optionally symmetrised by appending reversed pairs."""
+        optionally symmetrised by appending reversed pairs (SURVEY §8d);
+        permute=True relabels the ids by a fixed bijection (no reference
+        counterpart: robustness runs with hubs spread over the id space)."""
         st, inc = pcg_words(seed)
         h = ctypes.c_void_p()
         L.check(L.lib().abfs_graph_generate_rmat(device, scale, edges, a, b, c,
                                                  L.ptr(st, L.u64p), L.ptr(inc, L.u64p),
-                                                 int(symmetrize), ctypes.byref(h)),
+                                                 int(bool(symmetrize)) | (2 if permute else 0),
+                                                 ctypes.byref(h)),
                 "generate_rmat")
         return cls(h)
 

@@ -107,3 +107,24 @@ def test_reference_named_construction_routes_to_the_device(monkeypatch):
     assert isinstance(g, DeviceResidentGraph) and not isinstance(h, DeviceResidentGraph)
     for k in ("out_offsets", "destinations", "origins", "in_offsets", "sources"):
         np.testing.assert_array_equal(getattr(g, k), getattr(h, k), err_msg=k)
+
+
+def test_permuted_kronecker_is_the_relabelled_graph():
+    """bench.py --permute's graph: the same Kronecker edges with ids mapped by
+    v -> (v * 0x9E3779B1 + 0x7F4A7C15) mod 2^scale; BFS depths commute with
+    the relabelling (both level drivers, tree-switched)."""
+    scale = 12
+    base = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True)
+    perm = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True, permute=True)
+    ids = ((np.arange(1 << scale, dtype=np.uint64) * 0x9E3779B1 + 0x7F4A7C15) &
+           np.uint64((1 << scale) - 1)).astype(np.int64)
+    assert np.unique(ids).size == 1 << scale
+    ob, _ = base.offsets()
+    op, _ = perm.offsets()
+    np.testing.assert_array_equal(np.diff(op.astype(np.int64))[ids], np.diff(ob.astype(np.int64)))
+    gb, gp = base.to_graph(), perm.to_graph()
+    flat = P.deserialize(G.tree_path("t1"))
+    for r in (0, 5, 777):
+        want = P.reference_bfs(gb, r)
+        d, _ = P.adaptive_bfs(gp, int(ids[r]), flat, P.compute_stats(gp))
+        np.testing.assert_array_equal(d[ids], want)
