@@ -173,3 +173,24 @@ def test_generated_partitions_bfs_equal_single_gpu_engine():
         assert [(int(x.kernel), int(x.variant), x.frontier_size) for x in tr.records] == \
                [(x.kernel, x.variant, x.frontier_size) for x in recs]
         np.testing.assert_array_equal(bfs.depths(), want)
+
+
+def test_multi_gpu_bench_runs_end_to_end_with_ranks_sharing_one_gpu():
+    """bench.py --gpus 2 under torchrun (the driver's SCALE launch) with both
+    ranks on GPU 0 (--shared-gpu: gloo control plane; slices from the
+    generator stream; fused peer exchange over CUDA IPC): one JSON line."""
+    import json
+    import subprocess
+    import sys
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+           "--shared-gpu", "--scale", "14", "--steps", "1", "--warmup", "3",
+           "--roots-per-step", "2"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+    assert "1-D edge-balanced" in d["config"]["parallelism"]

@@ -44,6 +44,24 @@ def worker(rank, world, port, q):
                 checked += 1
             dist.barrier()
             part.close()
+        # slices built from the generator stream on each rank (bench --gpus N path)
+        from paper_1708_01159_b200.partition import gen_offsets, gen_spec
+        spec = gen_spec("rmat", scale=12, edges=16 << 12, seed=1, symmetrize=True)
+        oo, io = gen_offsets(spec, 0)
+        bounds = edge_balanced_bounds(io, world)
+        part = DevicePartition(None, int(bounds[rank]), int(bounds[rank + 1]),
+                               torch.cuda.current_stream().cuda_stream, spec=spec, device=0)
+        bfs = PartitionedBFS([part], bounds, DistPeerExchange(torch, dist, part), alloc=None)
+        stats = stats_from_offsets(1 << 12, 32 << 12, oo, io)
+        host = DeviceGraph.rmat(12, 16 << 12, 1, symmetrize=True).to_graph()
+        flat = P.deserialize(os.path.join(ROOT, "models", "gpu_tree.tree"))
+        cand = np.flatnonzero(np.diff(oo.astype(np.int64)) > 0)
+        for r in (int(cand[0]), int(cand[len(cand) // 2]), int(cand[-1])):
+            bfs.adaptive(r, flat, stats)
+            np.testing.assert_array_equal(bfs.depths(), P.reference_bfs(host, r))
+            checked += 1
+        dist.barrier()
+        part.close()
         q.put((rank, "ok", checked))
     except Exception:
         q.put((rank, traceback.format_exc(), 0))
