@@ -782,6 +782,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.init_in_kernel = host_init ? 0 : 1;
     P.solo_ctas = t->mega_cluster ? (uint32_t)t->mega_cluster : 0u;
     P.solo = t->dsolo;
+    P.solo_passes = (uint32_t)env_u64("ABFS_SOLO_PASSES", 2);   // mesh 4096^2: 2 passes -9 % vs 1
     P.part = 0;
     P.m_rev = g.m;
     P.lo = 0;

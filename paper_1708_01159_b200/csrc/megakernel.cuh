@@ -63,6 +63,7 @@ struct MegaParams {
     // top-down levels execute on cluster 0 alone (solo_ctas CTAs, cluster
     // barriers) while the other CTAs wait at one grid barrier
     uint32_t solo_ctas;
+    uint32_t solo_passes;       // frontier passes of the cluster's threads a solo level may take
     struct SoloState *solo;
     // ---- vertex partition (part = 1; partition.cu): this rank owns
     // destinations [lo, hi); depth / visited / noin / in_off / first_src are
@@ -318,7 +319,7 @@ __device__ __forceinline__ void solo_light(const MegaParams &P, const LevelCtx &
 __device__ __forceinline__ bool solo_fits(const MegaParams &P, int kernel,
                                           unsigned long long frontier) {
     // one pass of the cluster's threads (two for virtual warps)
-    const unsigned long long lanes = (unsigned long long)P.solo_ctas * kBlock;
+    const unsigned long long lanes = (unsigned long long)P.solo_ctas * kBlock * P.solo_passes;
     if (kernel == 2) return frontier <= lanes;
     // virtual warps: two passes pay off for wide warps (few vertices per
     // pass); narrow ones (a degree-fitted width of 1-2 lanes) are push-like
