@@ -678,8 +678,10 @@ def run_multi(a):
 
     # ---- secondary: the same BFS with the NCCL all-gather exchange --------
     nccl = None
-    if not a.no_secondary:
+    if a.nccl_line and not a.no_secondary:
+      try:
         from paper_1708_01159_b200.partition import DistExchange, PartitionedBFS
+        torch.cuda.set_stream(run.stream)   # the all-gathers must follow the levels' kernels
         nb = PartitionedBFS([run.part], run.bounds, DistExchange(torch, dist),
                             alloc=lambda s: torch.zeros(s, dtype=torch.int32, device=f"cuda:{local}"))
         nb.time_exchange = True
@@ -702,22 +704,27 @@ def run_multi(a):
                 "bytes_received_per_rank_per_level": int(nrecv),
                 "GBps_received_per_rank": round(nrecv / (ex_us * 1e-6) / 1e9, 2) if ex_us else None,
                 "nvlink_peak_GBps_per_direction": 900.0, "roots": len(sample)}
+      except Exception as exc:   # a secondary line never costs the headline
+        nccl = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+      finally:
+        torch.cuda.set_stream(torch.cuda.default_stream(local))
 
     # ---- secondary: config 3 (Kronecker-26) over the same partition -------
     k26 = None
+    run.close()
     if not a.no_secondary and a.graph == "kronecker" and a.scale != 26:
-        run.close()
-        r26 = PartitionedRun(torch, dist, a, "kronecker", 26, "peer", local)
-        m26 = {r: r26.traversed(r, flat)[0] for r in r26.roots[:4]}
-        o26 = [r26.roots[i % 4] for i in range(8)]
-        ms26 = r26.time_roots(o26, flat)
-        k26 = {"workload": r26.wname, "vertices": r26.V, "directed_edge_slots": r26.E,
-               "gteps": round(sum(m26[r] for r in o26) / (ms26 * 1e-3) / 1e9, 3),
-               "ms_per_bfs": round(ms26 / len(o26), 4), "bfs_timed": len(o26),
-               "setup_s": round(r26.setup_s, 1)}
-        r26.close()
-    else:
-        run.close()
+        try:
+            r26 = PartitionedRun(torch, dist, a, "kronecker", 26, "peer", local)
+            m26 = {r: r26.traversed(r, flat)[0] for r in r26.roots[:4]}
+            o26 = [r26.roots[i % 4] for i in range(8)]
+            ms26 = r26.time_roots(o26, flat)
+            k26 = {"workload": r26.wname, "vertices": r26.V, "directed_edge_slots": r26.E,
+                   "gteps": round(sum(m26[r] for r in o26) / (ms26 * 1e-3) / 1e9, 3),
+                   "ms_per_bfs": round(ms26 / len(o26), 4), "bfs_timed": len(o26),
+                   "setup_s": round(r26.setup_s, 1)}
+            r26.close()
+        except Exception as exc:
+            k26 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0:
         line = {
@@ -886,6 +893,9 @@ def main():
     ap.add_argument("--shared-gpu", action="store_true",
                     help="N > 1 test mode: all ranks on GPU 0 (gloo control plane; the peer "
                          "exchange still runs through CUDA IPC)")
+    ap.add_argument("--nccl-line", action="store_true",
+                    help="N > 1: also time the BFS with the NCCL all-gather exchange (per-level "
+                         "launches + all_gather_into_tensor; not verifiable on a one-GPU box)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="N > 1: skip the NCCL-exchange and Kronecker-26 secondary lines")
     ap.add_argument("--mode", type=int, default=1,
