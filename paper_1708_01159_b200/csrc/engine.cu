@@ -825,7 +825,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     // the offsets their probe just loaded), kept tested for the carried-list
     // tail levels it does speed up
     P.pl_s = P.pl_c0 = P.pl_c1 = nullptr;
-    if (env_u64("ABFS_PULL2", 0) && g.n < (1ull << 31)) {
+    if (ABFS_PULL2_CODE && env_u64("ABFS_PULL2", 0) && g.n < (1ull << 31)) {
         if (!t->pl) ABFS_CUDA(cudaMalloc((void **)&t->pl, 3 * (g.n + 4) * sizeof(uint32_t)));
         P.pl_s = t->pl;
         P.pl_c0 = t->pl + (g.n + 4);

@@ -19,6 +19,10 @@
 #include <vector>
 
 #include "bfs_kernels.cuh"
+#ifndef ABFS_PULL2_CODE
+#define ABFS_PULL2_CODE 0   // the list-based pull (pull2.cuh) in the megakernel: opt-in build,
+                            // it costs the default path registers even when unused
+#endif
 #include "pull2.cuh"
 
 namespace abfs {
@@ -260,6 +264,7 @@ __device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx
         return c.acc ? kStratBitmap : 0;
     }
     case 3:
+#if ABFS_PULL2_CODE
         if (PL) {
             // list-based pull: probe 0 grid-wide, then the survivors' scans
             CEmit<VAR> em(sn, c.count);
@@ -286,6 +291,7 @@ __device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx
             pull_heavy_body(c, s_done, P.in_off, P.src, fbm_next);
             break;
         }
+#endif
         {
             // the pull scratch lists alias the (idle) CTA queue buffer
             static_assert(sizeof(uint32_t) * kWarps * kPullList <= sizeof(sq->buf), "pull list");

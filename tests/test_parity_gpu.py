@@ -7,6 +7,8 @@ adaptive trace (kernel, variant, fallback, frontier) given the same tree.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 from hypothesis import given, settings
@@ -506,6 +508,10 @@ def test_red_mode_batch_checksums_k18(red_mode):
     t.close()
 
 
+@pytest.mark.skipif(os.environ.get("ABFS_TEST_PULL2_BUILD") != "1",
+                    reason="list-based pull is an opt-in build (-DABFS_PULL2_CODE=1 via "
+                           "tools/build_variant.sh; run with ABFS_LIB=<that build> and "
+                           "ABFS_TEST_PULL2_BUILD=1)")
 @pytest.mark.parametrize("name", NAMES)
 def test_list_pull_all_pairs_and_traces_match_reference(name, monkeypatch):
     """The megakernel's list-based pull (pull2.cuh, ABFS_PULL2=1: grid-wide
