@@ -90,6 +90,7 @@ struct abfs_traversal {
     int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
     SoloState *dsolo = nullptr; // solo-mode hand-off (device)
     int mega_minb = kMegaMinB;  // resident CTAs per SM the megakernel is compiled for
+    void *mega_kfn = nullptr;   // the megakernel instantiation mega_grid was sized for
     char *stage = nullptr;                     // pinned D2H staging (2 chunks)
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
@@ -635,7 +636,7 @@ int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device) {
     static int grids[64] = {0};
     if (device < 0 || device >= 64) return fail(ABFS_EINVAL, "device ordinal out of range");
     int &grid = grids[device];
-    void *kfn = (void *)k_mega<kMegaMinB>;
+    void *kfn = (void *)k_mega<kMegaMinB, true>;
     if (!grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -669,13 +670,26 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaMalloc((void **)&t->dsums, kMaxBatch * sizeof(unsigned long long)));
     }
     if (nroots < 1 || nroots > kMaxBatch) return fail(ABFS_EINVAL, "bad root count");
+    // cluster solo mode only on graphs without hubs (max out-degree <=
+    // kPushHub): there no small level ever needs CTA units, so solo levels
+    // never hand back; on skewed graphs the cluster-constrained grid and hub
+    // hand-backs cost more than the solo levels save (measured on
+    // Kronecker-24).  The kernel without solo code spills less (224 / 340 B
+    // instead of 260 / 504 B).
+    const char *solo_env = getenv("ABFS_SOLO");
+    const bool want_solo = solo_env ? atoi(solo_env) != 0 : t->max_out_degree <= kPushHub;
 #ifdef ABFS_MEGA_VARIANTS   // occupancy experiments (set_mode 2 / 3)
-    void *kfn = t->mega_minb == 4   ? (void *)k_mega<4>
-                : t->mega_minb == 6 ? (void *)k_mega<6>
-                                    : (void *)k_mega<kMegaMinB>;
+    void *kfn = t->mega_minb == 4   ? (void *)k_mega<4, false>
+                : t->mega_minb == 6 ? (void *)k_mega<6, false>
+                                    : (void *)k_mega<kMegaMinB, false>;
 #else
-    void *kfn = (void *)k_mega<kMegaMinB>;
+    void *kfn = want_solo ? (void *)k_mega<kMegaMinB, false, true>
+                          : (void *)k_mega<kMegaMinB, false, false>;
 #endif
+    if (t->mega_kfn != kfn) {   // e.g. ABFS_SOLO toggled: re-size the grid
+        t->mega_kfn = kfn;
+        t->mega_grid = 0;
+    }
     if (!t->mega_grid) {
         int per = 0, sms = 0;
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
@@ -685,13 +699,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         t->mega_cluster = 0;
         // cluster launch for solo mode: the grid must be whole clusters that
         // are all co-resident (cooperative)
-        // only on graphs without hubs (max out-degree <= kPushHub): there no
-        // small level ever needs CTA units, so solo levels never hand back;
-        // on skewed graphs the cluster-constrained grid and hub hand-backs
-        // cost more than the solo levels save (measured on Kronecker-24)
-        const char *env = getenv("ABFS_SOLO");
-        const bool want = env ? atoi(env) != 0 : t->max_out_degree <= kPushHub;
-        if (want) {
+        if (want_solo) {
             cudaLaunchConfig_t cfg = {};
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;

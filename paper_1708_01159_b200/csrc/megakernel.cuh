@@ -340,7 +340,9 @@ constexpr int kMegaMinB = ABFS_MEGA_MINB;   // default variant (set_mode 1)
 
 // MINB = resident CTAs per SM the register budget is sized for (6 -> 40
 // registers, 4 -> 64); latency-bound pull levels want the higher occupancy.
-template <int MINB>
+// PART: the partition (one rank's slice, fused exchange) instantiation; the
+// single-graph one carries none of the partition code (fewer live registers)
+template <int MINB, bool PART, bool SOLO = true>
 __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ SmemQ sq;
     __shared__ uint32_t pfound[kWarps * kPullSub];
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
         const uint64_t nt = (uint64_t)gridDim.x * kBlock;
         const bool owned = root >= P.lo && root < P.hi;
-        if (!P.part) {
+        if (!PART) {
             const uint64_t n4 = P.n / 4;
             const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
             for (uint64_t i = tid; i < n4; i += nt) reinterpret_cast<int4 *>(P.depth)[i] = inf4;
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
             const uint32_t bits = (owned && w == (root >> 5)) ? 1u << (root & 31) : 0u;
             P.visited[w] = bits;
-            if (P.part) P.vprev[w - P.wlo] = bits;
+            if (PART) P.vprev[w - P.wlo] = bits;
         }
         for (uint64_t w = tid; w < P.words; w += nt) P.fbm0[w] = (w == (root >> 5)) ? 1u << (root & 31) : 0u;
         grid.sync();
@@ -440,7 +442,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             P.ctr->oe3[zero] = 0;
         }
         // (instrumented work-model runs take the grid path: it records N2 features)
-        if (P.solo_ctas && !P.instrument && has_q && level != solo_skip && solo_fits(P, pk, frontier)) {
+        if (SOLO && P.solo_ctas && !P.instrument && has_q && level != solo_skip &&
+            solo_fits(P, pk, frontier)) {
             // ---- cluster solo mode: cluster 0 runs this level and the
             // following small top-down levels alone (cluster barriers,
             // ~0.3 us) while every other CTA waits at ONE grid barrier
@@ -640,11 +643,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.zero_slot = zero;
         c.level = (int32_t)level;
         c.lvl1 = (int32_t)level + 1;
-        uint32_t *pull_next = P.part ? P.fnext : fbm_nxt;
+        uint32_t *pull_next = PART ? P.fnext : fbm_nxt;
         // list-based pull (single graph): sweep after a top-down level, the
         // carried candidate list after a pull level
         PullLists pl;
-        const bool use_pl = pk == 3 && P.pl_s && !P.part;
+        const bool use_pl = pk == 3 && P.pl_s && !PART;
         if (use_pl) {
             pl.s = P.pl_s;
             pl.c_in = pl_have >= 0 ? (pl_have ? P.pl_c1 : P.pl_c0) : nullptr;
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             pl_have = -1;
         }
         unsigned long long nw;
-        if (P.part) {
+        if (PART) {
             // fused frontier exchange: the visited bits this rank gained are
             // stored into every rank's next-frontier bitmap over peer memory,
             // then the ranks' counts are summed through the mailboxes
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         // N2 (instrumented runs only): sum of the out-degrees of this level's
         // discoveries -- the next frontier's out-edges -- reduced on the device
         unsigned long long next_oe = ~0ull;
-        if (P.instrument && !P.part) {
+        if (P.instrument && !PART) {
             const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
             const uint64_t nt = (uint64_t)gridDim.x * kBlock;
             unsigned long long acc = 0;
@@ -765,7 +768,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.t_end = globaltimer();
             // partitions: this rank's count through the level's count variant
             r.next_out_edges = next_oe;
-            r.scanned = P.part ? (topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
+            r.scanned = PART ? (topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
                                           : *(volatile unsigned long long *)&P.ctr->count[out])
                       : P.instrument ? *(volatile unsigned long long *)&P.ctr->es3[out] : 0ull;
         }
@@ -777,8 +780,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         frontier = nw;
         discovered += nw;
         cur ^= 1;
-        has_q = P.part ? false : topdown;   // a partition's next frontier is the gathered bitmap
-        has_bm = P.part ? true : (!topdown || (sflags & kStratBitmap));
+        has_q = PART ? false : topdown;   // a partition's next frontier is the gathered bitmap
+        has_bm = PART ? true : (!topdown || (sflags & kStratBitmap));
     }
     if (P.checksums) {
         // the traversal's last level ended at a grid barrier: every depth is final
