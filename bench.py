@@ -176,6 +176,18 @@ def make_graph(a, dev):
             f"kronecker-{a.scale}-ef16-symmetrised" + ("-permuted-ids" if a.permute else ""))
 
 
+def workload_config(a, wname, V, E, symmetric, R):
+    """The workload both arms time (identical dicts): graph, tree, root pool
+    and the step's roots -- implementation details live beside it."""
+    return {"workload": f"{wname} tree-switched BFS",
+            "graph": a.graph, "scale": a.scale, "vertices": V, "directed_edge_slots": E,
+            "teps_basis": "sum of out-degree of reached vertices" + (" / 2" if symmetric else ""),
+            "roots_per_step": R, "roots_pool": 64,
+            "root_order": "64 seeded non-isolated roots (seed 1); step s times roots "
+                          "[s*R, (s+1)*R) of the pool repeated, after the warm-up steps",
+            "model": os.path.relpath(a.model, ROOT)}
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -391,16 +403,13 @@ def run_ours(a):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (device-generated Kronecker, bit-exact to the reference generator"
                     + (", ids relabelled by a fixed bijection)" if a.permute else ")"),
-            "config": {"workload": f"{wname} tree-switched BFS",
-                       "graph": a.graph, "scale": a.scale, "vertices": V, "directed_edge_slots": E,
-                       "teps_basis": "sum of out-degree of reached vertices" + (" / 2" if symmetric else ""),
-                       "roots_per_step": R, "roots_pool": 64,
-                       "step": "abfs_adaptive_bfs_batch: R tree-switched BFSs (init_depths "
-                               "included) in one persistent launch",
-                       "level_loop": "device (persistent megakernel)" if a.mode else "host (per-level launches)",
-                       "model": os.path.relpath(a.model, ROOT),
-                       "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
-                       "l2": "inputs larger than L2 (graph arrays 8.1 GB)"},
+            "config": workload_config(a, wname, V, E, symmetric, R),
+            "implementation": {"step": "abfs_adaptive_bfs_batch: R tree-switched BFSs (init_depths "
+                                       "included) in one persistent launch",
+                               "level_loop": "device (persistent megakernel)" if a.mode
+                               else "host (per-level launches)",
+                               "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
+                               "l2": "inputs larger than L2 (graph arrays 8.1 GB)"},
             "gteps_graph500_tbfs": round(edges / (bfs_ns * 1e-9) / 1e9, 3) if world == 1 else None,
             "gteps_per_root": {"median": round(statistics.median(per_root), 3),
                                "harmonic_mean": round(len(per_root) / sum(1 / x for x in per_root), 3),
@@ -832,16 +841,20 @@ def run_reference(a):
                            flat.lefts, flat.rights, flat.leaf_classes)
     deg = np.diff(og.out_offsets.astype(np.int64))
     setup = time.time() - t0
-    vals, times = [], []
-    edges_tot, el_tot = 0.0, 0.0
+    # the same steps as the GPU arm: R roots per step, rotating through the
+    # 64-root pool in the same order, warm-up steps first
+    R = a.roots_per_step
+    order = [roots[i % len(roots)] for i in range(R * (a.warmup + a.steps))]
+    edges_tot, el_tot, times = 0.0, 0.0, []
     for s in range(a.warmup + a.steps):
-        r = roots[s % len(roots)]
         t1 = time.perf_counter()
-        d, _ = oracle.adaptive_bfs(og, r, ot, static24, threads=threads)
+        e_step = 0.0
+        for r in order[s * R:(s + 1) * R]:
+            d, _ = oracle.adaptive_bfs(og, r, ot, static24, threads=threads)
+            e_step += deg[d != 2**31 - 1].sum() / 2
         el = time.perf_counter() - t1
         if s >= a.warmup:
-            e = deg[d != 2**31 - 1].sum() / 2
-            edges_tot += e
+            edges_tot += e_step
             el_tot += el
             times.append(el)
     gteps = edges_tot / el_tot / 1e9
@@ -850,12 +863,13 @@ def run_reference(a):
             "ms_per_step": round(1e3 * el_tot / max(1, a.steps), 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (host-generated Kronecker, same generator/seed)",
-            "config": {"workload": f"kronecker-{a.scale}-ef16-symmetrised tree-switched BFS",
-                       "scale": a.scale, "roots_per_step": 1,
-                       "model": os.path.relpath(a.model, ROOT)},
+            "config": workload_config(a, f"kronecker-{a.scale}-ef16-symmetrised", og.n, og.m, True, R),
+            "implementation": {"step": f"{R} tree-switched BFSs per step, one after the other, "
+                                       "C+OpenMP port of the reference level kernels (oracle/)",
+                               "parallelism": f"{threads} host threads"},
             "cpu_baseline": {"value": round(gteps, 5), "unit": UNIT, "cores": threads,
                              "kind": "port", "cpu_model": cpu_model(), "numpy": np.__version__,
-                             "sample": f"1 tree-switched BFS per step ({a.steps} steps) on the "
+                             "sample": f"{R} tree-switched BFSs per step ({a.steps} steps) on the "
                                        f"full graph; C+OpenMP port of the reference kernels"},
             "e2e": {"value": round(gteps, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
