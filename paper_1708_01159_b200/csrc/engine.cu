@@ -88,6 +88,7 @@ struct abfs_traversal {
     uint64_t n_noin = 0;           // vertices of in-degree 0 (sparse-pull estimate)
     int mega_grid = 0;
     int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
+    int solo_req = 0;           // cluster size asked for when mega_grid was sized (ABFS_SOLO_CLUSTER)
     SoloState *dsolo = nullptr; // solo-mode hand-off (device)
     int mega_minb = kMegaMinB;  // resident CTAs per SM the megakernel is compiled for
     void *mega_kfn = nullptr;   // the megakernel instantiation mega_grid was sized for
@@ -686,8 +687,15 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     void *kfn = want_solo ? (void *)k_mega<kMegaMinB, false, true>
                           : (void *)k_mega<kMegaMinB, false, false>;
 #endif
-    if (t->mega_kfn != kfn) {   // e.g. ABFS_SOLO toggled: re-size the grid
+    // solo cluster size: 16 CTAs (non-portable; 4096 lanes, one pass over a
+    // mesh-4096 level where 8 CTAs need two: mesh 4096^2 -23 % time) on
+    // low-degree graphs, whose long diameters are runs of small levels; 8
+    // elsewhere (16-CTA clusters fit fewer CTAs per grid: 608 vs 740 on B200,
+    // which big levels pay)
+    const int solo_cl = (int)env_u64("ABFS_SOLO_CLUSTER", t->max_out_degree <= 8 ? 16 : 8);
+    if (t->mega_kfn != kfn || t->solo_req != solo_cl) {   // e.g. ABFS_SOLO toggled: re-size the grid
         t->mega_kfn = kfn;
+        t->solo_req = solo_cl;
         t->mega_grid = 0;
     }
     if (!t->mega_grid) {
@@ -700,22 +708,26 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         // cluster launch for solo mode: the grid must be whole clusters that
         // are all co-resident (cooperative)
         if (want_solo) {
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kSoloCluster;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3((unsigned)(t->mega_grid / kSoloCluster * kSoloCluster));
-            cfg.blockDim = dim3(kBlock);
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters > 0) {
-                t->mega_grid = std::min(t->mega_grid / kSoloCluster, nclusters) * kSoloCluster;
-                t->mega_cluster = kSoloCluster;
+            // (a refused 16-CTA cluster falls back to 8)
+            for (int cl = solo_cl; cl >= 8 && !t->mega_cluster; cl /= 2) {
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                if (cl > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                at[0].val.clusterDim.x = cl;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3((unsigned)(t->mega_grid / cl * cl));
+                cfg.blockDim = dim3(kBlock);
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int nclusters = 0;
+                if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters > 0) {
+                    t->mega_grid = std::min(t->mega_grid / cl, nclusters) * cl;
+                    t->mega_cluster = cl;
+                }
+                cudaGetLastError();
             }
-            cudaGetLastError();
         }
     }
     if (!t->dsolo) ABFS_CUDA(cudaMalloc(&t->dsolo, sizeof(SoloState)));

@@ -134,7 +134,6 @@ std::mutex &mega_mutex(int device);   // held from a megakernel launch to its co
 
 constexpr uint32_t kMegaCapPart = 1u << 16;   // level records of a partition's loop
 constexpr uint32_t kSoloUnits = 16;   // more CTA units than this: hand the level to the grid
-constexpr int kSoloCluster = 8;       // CTAs of cluster 0 (portable cluster size)
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -1,7 +1,7 @@
 """Per-level device times of tree-switched BFSs under several environment
 settings (A/B of engine knobs read per call, e.g. ABFS_RED_*):
 
-    python tools/level_ab.py [--graph kron|er|mesh] [--roots N] "ENV=a" "ENV=b" ...
+    python tools/level_ab.py [--graph kron|er|mesh] [--roots N] "ENV=a" "ENV=b;ENV2=c" ...
 
 Prints, per root and level, the pair, frontier and each setting's level time."""
 import argparse
@@ -37,9 +37,9 @@ t = Traversal(dg)
 roots = pick_roots(oo, 64, 1)[:a.roots]
 res = {}
 for s in a.settings:
-    k, v = s.split("=", 1)
-    old = os.environ.get(k)
-    os.environ[k] = v
+    kv = dict(x.split("=", 1) for x in s.split(";"))   # "A=1;B=2" sets several
+    old = {k: os.environ.get(k) for k in kv}
+    os.environ.update(kv)
     for r in roots:
         t.adaptive(r, tree, st, 32)
         best = None
@@ -48,10 +48,11 @@ for s in a.settings:
             ns = np.array([x.elapsed_ns for x in recs], np.float64)
             best = ns if best is None else np.minimum(best, ns)
         res[(s, r)] = (recs, best)
-    if old is None:
-        del os.environ[k]
-    else:
-        os.environ[k] = old
+    for k, v in old.items():
+        if v is None:
+            del os.environ[k]
+        else:
+            os.environ[k] = v
 tot = {s: 0.0 for s in a.settings}
 for r in roots:
     recs0 = res[(a.settings[0], r)][0]

@@ -1,7 +1,7 @@
 """Per-source-line instruction / divergence / stall-sample totals of one
 kernel in an ncu report (SASS page + nvdisasm line map of the same build).
 
-    python tools/ncu_lines.py report.ncu-rep <mangled kernel> [cubin]
+    python tools/ncu_lines.py report.ncu-rep <mangled kernel> [cubin [top [samples]]]
 """
 import collections, csv, re, subprocess, sys
 
@@ -47,6 +47,7 @@ for r in data:
         tot[k] += vals[k]
 print(f"warp inst {tot[0]/1e6:.1f}M thread inst {tot[1]/1e6:.1f}M avg threads/inst "
       f"{tot[1]/tot[0]:.1f} stall samples {tot[2]:.0f}")
-for ln, b in sorted(by.items(), key=lambda x: -x[1][0])[:int(sys.argv[4]) if len(sys.argv) > 4 else 40]:
+key = 2 if len(sys.argv) > 5 and sys.argv[5] == "samples" else 0   # sort by stall samples
+for ln, b in sorted(by.items(), key=lambda x: -x[1][key])[:int(sys.argv[4]) if len(sys.argv) > 4 else 40]:
     print(f"{ln}  inst {b[0]/1e6:6.2f}M ({100*b[0]/tot[0]:4.1f}%)  threads/inst {b[1]/max(b[0],1):4.1f}"
-          f"  samples {100*b[2]/tot[2]:4.1f}%")
+          f"  samples {100*b[2]/tot[2]:4.1f}% ({b[2]:.0f})")

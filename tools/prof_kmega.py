@@ -5,6 +5,8 @@ cudaProfilerStart/Stop, so ncu captures exactly the kernel bench.py times:
     ncu --profile-from-start off --set full --clock-control none \
         --import-source on -k regex:k_mega -o gpurun_out/kmega \
         python tools/prof_kmega.py [R] [first_root_index]
+
+ABFS_PROF_GRAPH=mesh profiles the 4096^2 mesh (config 4) instead.
 """
 import os
 import sys
@@ -20,7 +22,10 @@ from paper_1708_01159_b200.features import static_vector  # noqa: E402
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 first = int(sys.argv[2]) if len(sys.argv) > 2 else 24   # bench's first timed step: roots 24..31
 scale = int(os.environ.get("ABFS_PROF_SCALE", "24"))
-dg = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True)
+if os.environ.get("ABFS_PROF_GRAPH") == "mesh":   # config 4 (ABFS_PROF_GRAPH=mesh, R=1)
+    dg = DeviceGraph.mesh(4096, 4096)
+else:
+    dg = DeviceGraph.rmat(scale, 16 << scale, 1, symmetrize=True)
 oo, _ = dg.offsets()
 stats = P.compute_stats(dg)
 tree = P.deserialize(default_model()).as_abfs()
