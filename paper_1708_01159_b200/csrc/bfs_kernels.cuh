@@ -38,7 +38,9 @@ namespace abfs {
 // count into counts[parity][rank].
 struct PeerBox {
     unsigned long long arrive;
-    unsigned long long pad[7];
+    unsigned long long mk_arrive;     // megakernel exchanges: 2^32 per rank per exchange
+    unsigned long long mk_sum[3];     // megakernel exchanges: level count, rotating slots
+    unsigned long long pad[3];
     unsigned long long counts[2][64];
     unsigned long long local;      // this rank's own count (accumulator)
     unsigned int timeout;          // set if a wait gave up

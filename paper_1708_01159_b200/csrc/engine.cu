@@ -816,8 +816,6 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.box = nullptr;
     P.nranks = 0;
     P.rank = 0;
-    P.xcount = nullptr;
-    P.gcount = nullptr;
     P.xseq0 = 0;
     P.checksums = nullptr;
     if (checksums) {

@@ -86,9 +86,8 @@ struct MegaParams {
     PeerBox *const *peer_box;   // [nranks]
     PeerBox *box;
     uint32_t nranks, rank;
-    unsigned long long *xcount; // slice popc accumulator
-    unsigned long long *gcount; // global level count of the last exchange
-    unsigned long long xseq0;   // exchanges completed before this launch
+    unsigned long long xseq0;   // megakernel exchanges completed before this launch (PeerBox::mk_*)
+    int xsys;                   // a peer is on another GPU: system-scope exchange signalling
     // optional [nroots]: per-root depth checksum (depth_mix) of the final
     // depth array of each traversal, for batch parity checks
     unsigned long long *checksums;
@@ -351,6 +350,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ int s_cls;
     __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned s_base;
+    __shared__ unsigned long long s_nw;   // partition mode: the exchanged level count
     __shared__ __align__(16) CutNode s_tree[kMegaTreeNodes];
     cg::grid_group grid = cg::this_grid();
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -656,6 +656,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         }
         const unsigned long long settled = discovered + P.n_noin;
         const bool wide = P.pull_wide_max && (settled >= P.n || P.n - settled <= P.pull_wide_max);
+#ifdef ABFS_DIAG_PART
+        unsigned long long tdg = 0;
+        if (ABFS_DIAG_PART == 1 && lead) tdg = globaltimer();   // after conversions
+#endif
         int sflags;
         switch (pv) {
         case 0: sflags = mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, s_fetch, warp_tot, &s_base, wide, use_pl ? &pl : nullptr, pl_n, grid); break;
@@ -670,6 +674,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             pl_have = -1;
         }
         unsigned long long nw;
+#ifdef ABFS_DIAG_PART
+        if (ABFS_DIAG_PART == 2 && lead) tdg = globaltimer();   // after the strategy
+#endif
         if (PART) {
             // fused frontier exchange: the visited bits this rank gained are
             // stored into every rank's next-frontier bitmap over peer memory,
@@ -687,37 +694,63 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
-            if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(P.xcount, cnt);
-            __threadfence_system();   // this thread's peer stores before the signal
-            grid.sync();
-            if (lead) {
-                __threadfence_system();
-                const unsigned long long tot = *(volatile unsigned long long *)P.xcount;
-                *(volatile unsigned long long *)P.xcount = 0;
-                const int par = (int)(xseq & 1);
-                for (uint32_t r = 0; r < P.nranks; ++r)
-                    *(volatile unsigned long long *)&P.peer_box[r]->counts[par][P.rank] = tot;
-                __threadfence_system();
-                for (uint32_t r = 0; r < P.nranks; ++r) atomicAdd_system(&P.peer_box[r]->arrive, 1ull);
-                const unsigned long long expect = (xseq + 1) * P.nranks, tw = globaltimer();
+            if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = (unsigned)cnt;
+            __syncthreads();
+#ifdef ABFS_DIAG_PART
+            if (ABFS_DIAG_PART == 3 && lead) tdg = globaltimer();   // after the scan
+#endif
+            // one cross-rank round per level, per CTA (no grid barrier, no
+            // lead-only phase): each CTA adds its slice count into every
+            // rank's mailbox sum and releases its arrival at system scope
+            // (cumulative over the CTA's peer stores through the CTA
+            // barrier), then waits for every CTA of every rank.  A rank's CTAs
+            // add weights summing to exactly 2^32 per exchange, whatever its
+            // grid size.  The release / acquire pair is system-scoped when a
+            // peer bitmap lives on another GPU (xsys) and GPU-scoped when
+            // every rank shares this device (P = 1, ranks sharing a GPU): a
+            // system-scope release costs ~6 us per level on B200, a GPU-scope
+            // one ~1 us.  Sums rotate over 3 slots: slot (x+1)%3 is cleared
+            // by this rank before it signals exchange x, and no peer adds to
+            // it before seeing that signal.
+            if (threadIdx.x == 0) {
+                unsigned long long s = 0;
+                for (int w = 0; w < kWarps; ++w) s += warp_tot[w];
+                const uint32_t slot = (uint32_t)(xseq % 3);
+                if (lead) P.box->mk_sum[(xseq + 1) % 3] = 0;
+                const unsigned long long b = blockIdx.x, G = gridDim.x;
+                const unsigned long long wgt = ((b + 1) << 32) / G - (b << 32) / G;
+                for (uint32_t r = 0; r < P.nranks; ++r) {
+                    if (s) atomicAdd_system(&P.peer_box[r]->mk_sum[slot], s);
+                    if (P.xsys)
+                        asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
+                                     "l"(wgt) : "memory");
+                    else
+                        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
+                                     "l"(wgt) : "memory");
+                }
+                const unsigned long long expect = ((xseq + 1) * P.nranks) << 32, tw = globaltimer();
                 bool ok = true;
-                while (*(volatile unsigned long long *)&P.box->arrive < expect) {
+                for (;;) {
+                    unsigned long long a;
+                    if (P.xsys)
+                        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
+                    else
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
+                    if (a >= expect) break;
                     if (globaltimer() - tw > 20000000000ull) {   // a rank never arrived
                         P.box->timeout = 1;
                         ok = false;
                         break;
                     }
-                    __nanosleep(100);
+                    __nanosleep(32);
                 }
-                __threadfence_system();
                 unsigned long long g = 0;
-                for (uint32_t r = 0; r < P.nranks; ++r)
-                    g += *(volatile unsigned long long *)&P.box->counts[par][r];
-                *(volatile unsigned long long *)P.gcount = ok ? g : 0ull;   // 0 ends the traversal
+                if (ok) g = *(volatile unsigned long long *)&P.box->mk_sum[slot];
+                s_nw = g;   // 0 ends the traversal
             }
             ++xseq;
-            grid.sync();
-            nw = *(volatile unsigned long long *)P.gcount;
+            __syncthreads();
+            nw = s_nw;
         } else {
             nw = topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
                          : *(volatile unsigned long long *)&P.ctr->count[out];
@@ -763,7 +796,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.frontier = frontier;
             r.new_count = nw;
             r.t_start = t0;
+#ifdef ABFS_DIAG_PART
+            r.t_pred = tdg;
+#else
             r.t_pred = tp;
+#endif
             r.t_end = globaltimer();
             // partitions: this rank's count through the level's count variant
             r.next_out_edges = next_oe;

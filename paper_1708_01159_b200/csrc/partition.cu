@@ -67,7 +67,9 @@ struct abfs_part {
     uint32_t **peer_fbm = nullptr;               // device [2][nranks] bitmap pointers
     PeerBox **peer_box = nullptr;                // device [nranks] mailbox pointers
     unsigned int *pack_ticket = nullptr;         // last-CTA ticket of the push kernel
-    unsigned long long p2p_seq = 0;              // exchanges done (every rank agrees)
+    unsigned long long p2p_seq = 0;              // launch-path exchanges done (every rank agrees)
+    unsigned long long mk_seq = 0;               // megakernel exchanges done (PeerBox::mk_*)
+    int x_sys = 1;                               // a peer buffer lives on another device
     std::vector<void *> ipc_opened;              // peer allocations mapped by IPC
     // persistent per-rank level loop (abfs_part_mega_*)
     uint32_t *q2 = nullptr;                      // second global-size queue
@@ -76,7 +78,6 @@ struct abfs_part {
     uint32_t *droots = nullptr;
     unsigned char *dtree = nullptr;
     size_t tree_cap = 0;
-    unsigned long long *dx = nullptr;            // {xcount, gcount}
 };
 
 namespace {
@@ -290,7 +291,6 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
     if (p->mnlev) cudaFreeHost(p->mnlev);
     cudaFree(p->droots);
     cudaFree(p->dtree);
-    cudaFree(p->dx);
     cudaFree(p->peer_fbm);
     cudaFree(p->peer_box);
     cudaFree(p->pack_ticket);
@@ -702,6 +702,17 @@ static int part_peers_common(abfs_part *p, uint32_t nranks, uint32_t rank,
     ABFS_CUDA(cudaMemcpy(p->peer_box, bx.data(), nranks * sizeof(PeerBox *), cudaMemcpyHostToDevice));
     p->nranks = nranks;
     p->rank = rank;
+    // every peer bitmap on this device (one process, or ranks sharing a GPU
+    // through IPC): the exchange can synchronise at GPU scope
+    int same = 1;
+    for (uint32_t q = 0; q < nranks && same; ++q) {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, f0[q]) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+            pa.device != p->device)
+            same = 0;
+    }
+    cudaGetLastError();
+    p->x_sys = same ? 0 : 1;
     return ABFS_OK;
 }
 
@@ -929,8 +940,6 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
         ABFS_CUDA(cudaHostAlloc((void **)&p->mnlev, sizeof(unsigned long long), cudaHostAllocMapped));
         ABFS_CUDA(cudaHostGetDevicePointer((void **)&p->dnlev, p->mnlev, 0));
         ABFS_CUDA(cudaMalloc(&p->droots, 16));
-        ABFS_CUDA(cudaMalloc(&p->dx, 2 * sizeof(unsigned long long)));
-        ABFS_CUDA(cudaMemset(p->dx, 0, 2 * sizeof(unsigned long long)));
     }
     std::vector<unsigned char> blob;
     uint32_t nn = 0;
@@ -994,9 +1003,11 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     P.box = p->box;
     P.nranks = p->nranks;
     P.rank = p->rank;
-    P.xcount = p->dx;
-    P.gcount = p->dx + 1;
-    P.xseq0 = p->p2p_seq;
+    P.xseq0 = p->mk_seq;
+    {
+        const char *xs = getenv("ABFS_XSYS");   // tests: force system-scope signalling
+        P.xsys = xs ? (atoi(xs) != 0) : p->x_sys;
+    }
     P.checksums = nullptr;
     P.acc = nullptr;   // RED-mode levels are single-graph only
     *(volatile unsigned long long *)p->mnlev = 0;
@@ -1009,7 +1020,7 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
         ABFS_CUDA(cudaStreamSynchronize(s));
     }
     const unsigned long long nl = *(volatile unsigned long long *)p->mnlev;
-    p->p2p_seq += nl;
+    p->mk_seq += nl;
     p->last_kernel = -1;
     p->has_q = false;
     int timed_out = 0;

@@ -93,6 +93,32 @@ def test_partitions_equal_single_gpu_engine(cfg, parts, exchange):
             np.testing.assert_array_equal(bfs.depths(), want)
 
 
+@pytest.mark.parametrize("xsys", ["0", "1"])
+def test_persistent_partition_loop_exchange_scopes(xsys, monkeypatch):
+    """The persistent per-rank loop signals each exchange at GPU scope when
+    every peer bitmap is on this device and at system scope otherwise
+    (ABFS_XSYS forces either); both must give the single-engine traversal."""
+    monkeypatch.setenv("ABFS_XSYS", xsys)
+    dg = DeviceGraph.rmat(18, 16 << 18, 1, symmetrize=True)
+    stats = P.compute_stats(dg)
+    flat = P.deserialize(MODEL)
+    t = Traversal(dg)
+    bfs = make_bfs(dg, 1, "peer")
+    assert bfs.persistent
+    oo, _ = dg.offsets()
+    cand = np.flatnonzero(np.diff(oo.astype(np.int64)) > 0)
+    for r in [int(cand[0]), int(cand[len(cand) // 2]), int(cand[-1])]:
+        want = np.empty(dg.vertex_count, np.int32)
+        recs = t.adaptive(r, flat.as_abfs(), static_vector(stats), 32, depths_out=want)
+        for _ in range(2):   # back-to-back launches continue the exchange sequence
+            tr = bfs.adaptive(r, flat, stats)
+            assert [(int(x.kernel), int(x.variant), x.frontier_size) for x in tr.records] == \
+                   [(x.kernel, x.variant, x.frontier_size) for x in recs]
+            np.testing.assert_array_equal(bfs.depths(), want)
+        outs = bfs.bfs_full(r, P.KernelId.VERTEX_PULL, P.CountVariant.GROUP_REDUCE)
+        assert sum(o.new_frontier_count for o in outs) + 1 == int((want != G.INF).sum())
+
+
 def test_partition_rejects_misaligned_range():
     n, m, a = G.graph_arrays("kron10")
     dg = DeviceGraph.upload(P.Graph(n, m, *[a[k].copy() for k in G.ARRAYS]))
