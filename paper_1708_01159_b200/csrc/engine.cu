@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "launch.cuh"
@@ -89,6 +90,9 @@ struct abfs_traversal {
     int mega_grid = 0;
     int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
     int solo_req = 0;           // cluster size asked for when mega_grid was sized (ABFS_SOLO_CLUSTER)
+    int grid_div = 1;           // batch sub-traversal: 1/grid_div of the co-resident grid
+    bool is_sub = false;        // owned by a parent's split batch (the parent holds the device lock)
+    abfs_traversal *sub[kMaxSplit] = {};   // split batch: concurrent half-grid traversals
     SoloState *dsolo = nullptr; // solo-mode hand-off (device)
     int mega_minb = kMegaMinB;  // resident CTAs per SM the megakernel is compiled for
     void *mega_kfn = nullptr;   // the megakernel instantiation mega_grid was sized for
@@ -390,6 +394,7 @@ extern "C" int abfs_traversal_create(abfs_graph *g, abfs_traversal **out) {
 extern "C" void abfs_traversal_destroy(abfs_traversal *t) {
     if (!t) return;
     { ABFS_LOCK(t); }   // no call on this handle is in flight any more
+    for (abfs_traversal *u : t->sub) abfs_traversal_destroy(u);
     cudaSetDevice(t->device);
     if (t->stream) cudaStreamSynchronize(t->stream);
     cudaFree(t->depth);
@@ -703,7 +708,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
         ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
         if (per < 1) return fail(ABFS_ECUDA, "megakernel cannot be resident");
-        t->mega_grid = per * sms;
+        t->mega_grid = std::max(1, per * sms / t->grid_div);
         t->mega_cluster = 0;
         // cluster launch for solo mode: the grid must be whole clusters that
         // are all co-resident (cooperative)
@@ -722,8 +727,9 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
                 int nclusters = 0;
-                if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters > 0) {
-                    t->mega_grid = std::min(t->mega_grid / cl, nclusters) * cl;
+                if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess &&
+                    nclusters / t->grid_div > 0) {
+                    t->mega_grid = std::min(t->mega_grid / cl, nclusters / t->grid_div) * cl;
                     t->mega_cluster = cl;
                 }
                 cudaGetLastError();
@@ -858,7 +864,11 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         P.acc = t->acc;
     }
     for (size_t i = 0; i < nroots; ++i) ((volatile unsigned long long *)t->mnlev)[i] = 0;
-    std::lock_guard<std::mutex> mega_guard(g_mega_mu[t->device & 63]);
+    // one megakernel per device at a time (co-residency), except a split
+    // batch's sub-traversals: their parent holds the lock for all of them and
+    // their grids add up to one co-resident grid
+    std::unique_lock<std::mutex> mega_guard(g_mega_mu[t->device & 63], std::defer_lock);
+    if (!t->is_sub) mega_guard.lock();
     ABFS_CUDA(cudaEventRecord(t->et0, s));
     void *args[] = {&P};
     if (t->mega_cluster) {
@@ -882,7 +892,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
             int per = 0, sms = 0;
             ABFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kBlock, 0));
             ABFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device));
-            t->mega_grid = per * sms;
+            t->mega_grid = std::max(1, per * sms / t->grid_div);
             t->mega_cluster = 0;
             P.solo_ctas = 0;
             ABFS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(t->mega_grid), dim3(kBlock), args, 0, s));
@@ -1252,6 +1262,119 @@ extern "C" int abfs_host_unregister(void *ptr) {
     return ABFS_OK;
 }
 
+// ---- split batch --------------------------------------------------------------
+// A multi-root batch runs as S concurrent megakernels (S sub-traversals with
+// their own scratch and stream, each 1/S of the co-resident grid, roots dealt
+// round-robin).  Every level of a BFS is a grid-wide dependent chain; the
+// small top-down levels (a handful of vertices, ~5-30 us of barriers and
+// L2 round trips each) leave the GPU idle, and a big pull level on half the
+// grid runs only ~1.3x longer (latency-bound), so two traversals side by side
+// overlap one's small levels with the other's work (K24 bench batch: 2.24 ->
+// 1.92 ms wall in the first A/B).  Same per-root results: each root is one
+// unchanged single-traversal run.  ABFS_BATCH_SPLIT=1 disables.
+static int batch_ways(const abfs_traversal *t, size_t nroots) {
+    if (t->is_sub || t->instrument || nroots < 2) return 1;
+    const int s = (int)env_u64("ABFS_BATCH_SPLIT", 2);
+    return std::max(1, std::min({s, kMaxSplit, (int)nroots}));
+}
+
+static int batch_split(abfs_traversal *t, const std::vector<uint32_t> &r32, int S,
+                       const abfs_tree *tr, const double *static24, int64_t chunk,
+                       uint64_t *levels, uint64_t *bfs_ns, uint64_t *total_ns,
+                       uint64_t *checksums, uint64_t *new_counts, size_t counts_cap,
+                       size_t *n_counts) {
+    const size_t nroots = r32.size();
+    for (int k = 0; k < S; ++k) {
+        abfs_traversal *&u = t->sub[k];
+        if (u && u->grid_div != S) {
+            abfs_traversal_destroy(u);
+            u = nullptr;
+        }
+        if (!u) {
+            ABFS_TRY(abfs_traversal_create(t->g, &u));
+            u->is_sub = true;
+            u->grid_div = S;
+        }
+        u->mega_minb = t->mega_minb;
+    }
+    std::vector<std::vector<uint32_t>> rk(S);
+    for (size_t i = 0; i < nroots; ++i) rk[i % S].push_back(r32[i]);
+    std::vector<std::vector<uint64_t>> ck(S);
+    for (int k = 0; k < S; ++k) ck[k].assign(rk[k].size(), 0);
+    const cudaStream_t s = t->stream;
+    ABFS_CUDA(cudaSetDevice(t->device));
+    ABFS_TRY(ensure_events(t, 2));
+    uint64_t launches0 = 0;
+    for (int k = 0; k < S; ++k) launches0 += t->sub[k]->launches;
+    std::lock_guard<std::mutex> mega_guard(g_mega_mu[t->device & 63]);
+    // fork: the sub streams start after the caller's stream's prior work
+    ABFS_CUDA(cudaEventRecord(t->et0, s));
+    for (int k = 0; k < S; ++k) ABFS_CUDA(cudaStreamWaitEvent(t->sub[k]->stream, t->et0, 0));
+    std::vector<int> rc(S, ABFS_OK);
+    std::vector<std::string> err(S);
+    std::vector<size_t> nl(S, 0);
+    auto go = [&](int k) {
+        rc[k] = mega_run(t->sub[k], rk[k].data(), rk[k].size(), false, -1, tr, static24, chunk,
+                         &nl[k], checksums ? ck[k].data() : nullptr);
+        if (rc[k] != ABFS_OK) err[k] = abfs_last_error();
+    };
+    std::vector<std::thread> th;
+    for (int k = 1; k < S; ++k) th.emplace_back(go, k);
+    go(0);
+    for (auto &x : th) x.join();
+    for (int k = 0; k < S; ++k)
+        if (rc[k] != ABFS_OK) return fail(rc[k], err[k]);
+    // join: the caller's stream continues after every sub-traversal
+    for (int k = 0; k < S; ++k) ABFS_CUDA(cudaStreamWaitEvent(s, t->sub[k]->ev[1], 0));
+    ABFS_CUDA(cudaEventRecord(t->ev[1], s));
+    // the batch's final state on the parent: the last root's depths
+    const abfs_traversal *last = t->sub[(nroots - 1) % S];
+    ABFS_CUDA(cudaMemcpyAsync(t->depth, last->depth, t->g->d.n * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, s));
+    ABFS_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    ABFS_CUDA(cudaEventElapsedTime(&ms, t->et0, t->ev[1]));
+    t->last_trav_ns = (uint64_t)llround((double)ms * 1e6);
+    uint64_t launches1 = 0;
+    for (int k = 0; k < S; ++k) launches1 += t->sub[k]->launches;
+    t->launches += launches1 - launches0;
+    if (total_ns) *total_ns = t->last_trav_ns;
+    // per-root outputs in the caller's root order
+    std::vector<size_t> off(S, 0);
+    t->batch_levels.assign(nroots, 0);
+    size_t nc = 0;
+    bool counts_whole = true;
+    for (size_t i = 0; i < nroots; ++i) {
+        const abfs_traversal *u = t->sub[i % S];
+        const size_t j = i / S, li = (size_t)u->batch_levels[j], o = off[i % S];
+        off[i % S] += li;
+        t->batch_levels[i] = li;
+        if (levels) levels[i] = li;
+        if (checksums) checksums[i] = ck[i % S][j];
+        const bool kept = li && o + li <= u->batch_recs;
+        if (bfs_ns) {
+            uint64_t ns = 0;
+            if (kept) {
+                const MegaRecord &a = u->mrecs[o], &b = u->mrecs[o + li - 1];
+                ns = b.t_end > a.t_start ? b.t_end - a.t_start : 1;
+            }
+            bfs_ns[i] = ns;
+        }
+        // every root's per-level new counts, concatenated in root order, up
+        // to the first root whose records were not kept
+        counts_whole = counts_whole && kept;
+        for (size_t l = 0; counts_whole && l < li; ++l, ++nc)
+            if (new_counts && nc < counts_cap) new_counts[nc] = u->mrecs[o + l].new_count;
+    }
+    if (n_counts) *n_counts = nc;
+    t->batch_recs = 0;   // (the records live in the sub-traversals)
+    t->hrecs.clear();
+    t->F = 0;
+    t->expect_level = -1;
+    t->has_q = t->has_bm = false;
+    return ABFS_OK;
+}
+
 static int batch_impl(abfs_traversal *t, const int64_t *roots, size_t nroots,
                       const abfs_tree *tr, const double *static24, int64_t chunk,
                       uint64_t *levels, uint64_t *bfs_ns, uint64_t *total_ns,
@@ -1270,6 +1393,10 @@ static int batch_impl(abfs_traversal *t, const int64_t *roots, size_t nroots,
                                          std::to_string(t->g->d.n));
         r32[i] = (uint32_t)roots[i];
     }
+    const int S = batch_ways(t, nroots);
+    if (S > 1)
+        return batch_split(t, r32, S, tr, static24, chunk, levels, bfs_ns, total_ns, checksums,
+                           new_counts, counts_cap, n_counts);
     size_t nl = 0;
     ABFS_TRY(mega_run(t, r32.data(), nroots, false, -1, tr, static24, chunk, &nl, checksums));
     if (total_ns) *total_ns = t->last_trav_ns;

@@ -273,6 +273,39 @@ def test_adaptive_batch_matches_single_traversals(name):
     t.close()
 
 
+@pytest.mark.parametrize("name", ["kron12", "mesh64", "unreach"])
+def test_split_batch_equals_one_launch(name, monkeypatch):
+    """A batch split over S concurrent partial-grid megakernels (roots dealt
+    round-robin, ABFS_BATCH_SPLIT) returns the same per-root level counts,
+    depth checksums and per-level new counts, in the caller's root order, as
+    the single launch; the final depths are the last root's."""
+    from paper_1708_01159_b200 import DeviceGraph, Traversal
+    from paper_1708_01159_b200.features import static_vector
+    g = graph(name)
+    dg = DeviceGraph.upload(g)
+    flat = P.deserialize(G.tree_path("t1"))
+    st = static_vector(P.compute_stats(g))
+    roots = G.roots(name)
+    order = (roots * 4)[:7]
+    base = None
+    for ways in ("1", "2", "3", "4"):
+        monkeypatch.setenv("ABFS_BATCH_SPLIT", ways)
+        t = Traversal(dg)
+        for batch in (order, order[:1], order[:2]):
+            lv, sums, per = t.adaptive_batch_check(batch, flat.as_abfs(), st)
+            got = (lv.tolist(), [int(x) for x in sums], per)
+            if ways == "1":
+                base = base or {}
+                base[len(batch)] = got
+            else:
+                assert got == base[len(batch)], (ways, len(batch))
+            np.testing.assert_array_equal(t.read(), G.depth(name, batch[-1]))
+        lv, ns, tot = t.adaptive_batch(order, flat.as_abfs(), st)
+        assert (ns > 0).all() and tot > 0 and lv.tolist() == base[len(order)][0]
+        t.close()
+    dg.close()
+
+
 def _random_tree(rng, selection, values, depth):
     """Preorder FlatTree of the given depth; thresholds drawn from the exact
     feature values a traversal produces and their float64 neighbours (the
