@@ -217,6 +217,11 @@ def run_ours(a):
     trav.set_device_loop(a.mode)
     stream = torch.cuda.Stream(device=dev)
     trav.set_stream(stream.cuda_stream)
+    # the headline keeps per-BFS semantics (GTEPS over t_bfs):
+    # every batch is ONE full-grid launch, its BFSs back to back; the split
+    # batch (concurrent partial-grid launches) is timed after, as a
+    # throughput key
+    trav.set_batch_ways(1)
 
     # traversed edges per root (Graph500 undirected basis: Σ out-degree / 2)
     m_trav = {}
@@ -262,6 +267,31 @@ def run_ours(a):
         dist.all_reduce(ee)
         edges = float(ee.item())
     gteps = edges / (ms * 1e-3) / 1e9
+
+    # ---- multi-BFS throughput: the same steps as S concurrent launches ----
+    concurrent = None
+    if world == 1 and a.mode:
+        trav.set_batch_ways(0)
+        S = trav.batch_ways(R)
+        if S > 1:
+            for s in range(a.warmup):
+                trav.adaptive_batch(order[s * R:(s + 1) * R], tree, static24, 32)
+            c_edges = 0.0
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for s in range(a.warmup, a.warmup + a.steps):
+                batch = order[s * R:(s + 1) * R]
+                trav.adaptive_batch(batch, tree, static24, 32)
+                c_edges += sum(m_trav[r] for r in batch)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            c_ms = ev0.elapsed_time(ev1)
+            concurrent = {"value": round(c_edges / (c_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+                          "ms_per_step": round(c_ms / a.steps, 4), "ways": S,
+                          "basis": "the same steps' R BFSs dealt round-robin to S concurrent "
+                                   "persistent launches of 1/S of the grid (abfs_adaptive_bfs_batch "
+                                   "default): multi-BFS throughput, each BFS's own t_bfs is longer"}
+        trav.set_batch_ways(1)
 
     # ---- roofline of the dominant kernel (instrumented replay, untimed) ----
     peak, peak_kind = measured_peak_hbm()
@@ -314,6 +344,10 @@ def run_ours(a):
                 "algorithmic_bytes_per_launch": int(dom_bytes / max(1, per_kernel[dom][2])),
                 "whole_traversal_GBps": round(sum(v[1] for v in per_kernel.values()) /
                                               (total_ns * 1e-9) / 1e9, 1),
+                # the timed step's aggregate: R roots' algorithmic bytes over
+                # ms_per_step (the concurrent launches together)
+                "step_GBps": round(sum(v[1] for v in per_kernel.values()) /
+                                   (ms / a.steps * 1e-3) / 1e9, 1) if world == 1 else None,
                 "timed_kernel_ncu": kmega}
 
     # ---- every fixed pair vs the switched run (same roots, untimed extra) ----
@@ -405,7 +439,7 @@ def run_ours(a):
                     + (", ids relabelled by a fixed bijection)" if a.permute else ")"),
             "config": workload_config(a, wname, V, E, symmetric, R),
             "implementation": {"step": "abfs_adaptive_bfs_batch: R tree-switched BFSs (init_depths "
-                                       "included) in one persistent launch",
+                                       "included) back to back in one persistent full-grid launch",
                                "level_loop": "device (persistent megakernel)" if a.mode
                                else "host (per-level launches)",
                                "parallelism": f"roots sharded over {world} GPU(s), graph replicated",
@@ -416,6 +450,7 @@ def run_ours(a):
                                "bfs": len(per_root)} if per_root else None,
             "fixed_vs_switched": fixed_block,
             "gpu_launches": int(launches),
+            "concurrent_batch": concurrent,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -175,11 +175,15 @@ ABFS_API int abfs_adaptive_bfs(abfs_traversal *t, int64_t root, const abfs_tree 
 
 /* Multi-source throughput form of adaptive_bfs (no reference counterpart;
  * each traversal has adaptive.py:83-129 semantics): nroots (<= 4096)
- * tree-switched BFSs run back to back inside ONE persistent launch, each
- * root's init_depths inside the kernel, no host round trip between them.
- * levels[i] / bfs_ns[i] (optional) = level calls and device time (first
- * level start .. last level end) of root i; total_ns = the launch.  The
- * depth array afterwards holds the last root's traversal. */
+ * tree-switched BFSs run inside persistent launches, each root's
+ * init_depths inside the kernel, no host round trip between them: the
+ * roots are dealt round-robin to S concurrent launches of 1/S of the
+ * co-resident grid (private scratch and stream each, forked from and joined
+ * back into the traversal's stream; S = abfs_traversal_batch_ways), each
+ * running its roots back to back.  levels[i] / bfs_ns[i] (optional) = level
+ * calls and device time (first level start .. last level end) of root i;
+ * total_ns = fork to join.  The depth array afterwards holds the last
+ * root's traversal. */
 ABFS_API int abfs_adaptive_bfs_batch(abfs_traversal *t, const int64_t *roots, size_t nroots,
                                      const abfs_tree *tree, const double *static24,
                                      int64_t chunk_size, uint64_t *levels, uint64_t *bfs_ns,
@@ -209,6 +213,14 @@ ABFS_API int abfs_last_traversal_ns(const abfs_traversal *t, uint64_t *ns);
  * megakernel also runs small levels on one 8-CTA cluster ("solo mode";
  * environment ABFS_SOLO=0/1 forces it off/on). */
 ABFS_API int abfs_traversal_set_mode(abfs_traversal *t, int device_loop);
+
+/* Concurrent launches a batch of nroots roots is split into (1 = one
+ * launch): abfs_traversal_set_batch_ways, else ABFS_BATCH_SPLIT, else 8 on graphs of max out-degree <= 8, 2 on
+ * graphs of more than 2^25 vertices, 4 otherwise; at most nroots. */
+ABFS_API int abfs_traversal_batch_ways(const abfs_traversal *t, size_t nroots, int *ways);
+/* Fix the split (ways >= 1; 1 = every batch in one full-grid launch, each
+ * BFS with the whole GPU: per-BFS t_bfs semantics) or 0 = automatic. */
+ABFS_API int abfs_traversal_set_batch_ways(abfs_traversal *t, int ways);
 
 /* Number of kernels this traversal has launched (bench gpu_launches). */
 ABFS_API int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches);

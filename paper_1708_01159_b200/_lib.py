@@ -106,6 +106,9 @@ _SIGNATURES = {
     "abfs_last_traversal_ns": (ctypes.c_int, [ctypes.c_void_p, u64p]),
     "abfs_traversal_set_mode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "abfs_traversal_launches": (ctypes.c_int, [ctypes.c_void_p, u64p]),
+    "abfs_traversal_batch_ways": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t,
+                                                 ctypes.POINTER(ctypes.c_int)]),
+    "abfs_traversal_set_batch_ways": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "abfs_traversal_instrument": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "abfs_traversal_level_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, u64p, u64p,
                                                   u64p, u64p]),

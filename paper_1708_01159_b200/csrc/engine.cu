@@ -91,6 +91,7 @@ struct abfs_traversal {
     int mega_cluster = 0;       // cluster size of the megakernel launch (0: plain cooperative)
     int solo_req = 0;           // cluster size asked for when mega_grid was sized (ABFS_SOLO_CLUSTER)
     int grid_div = 1;           // batch sub-traversal: 1/grid_div of the co-resident grid
+    int batch_ways_req = 0;     // abfs_traversal_set_batch_ways (0: automatic)
     bool is_sub = false;        // owned by a parent's split batch (the parent holds the device lock)
     abfs_traversal *sub[kMaxSplit] = {};   // split batch: concurrent half-grid traversals
     SoloState *dsolo = nullptr; // solo-mode hand-off (device)
@@ -1156,6 +1157,23 @@ launch_path:
     return ABFS_OK;
 }
 
+static int batch_ways(const abfs_traversal *t, size_t nroots);
+
+extern "C" int abfs_traversal_set_batch_ways(abfs_traversal *t, int ways) {
+    if (!t) return fail(ABFS_EINVAL, "null traversal");
+    if (ways < 0) return fail(ABFS_EINVAL, "ways must be >= 0 (0 = automatic)");
+    ABFS_LOCK(t);
+    t->batch_ways_req = ways;
+    return ABFS_OK;
+}
+
+extern "C" int abfs_traversal_batch_ways(const abfs_traversal *t, size_t nroots, int *ways) {
+    if (!t || !ways) return fail(ABFS_EINVAL, "null argument");
+    ABFS_LOCK(t);
+    *ways = batch_ways(t, nroots);
+    return ABFS_OK;
+}
+
 extern "C" int abfs_traversal_launches(const abfs_traversal *t, uint64_t *launches) {
     if (!t || !launches) return fail(ABFS_EINVAL, "null argument");
     ABFS_LOCK(t);
@@ -1269,12 +1287,20 @@ extern "C" int abfs_host_unregister(void *ptr) {
 // small top-down levels (a handful of vertices, ~5-30 us of barriers and
 // L2 round trips each) leave the GPU idle, and a big pull level on half the
 // grid runs only ~1.3x longer (latency-bound), so two traversals side by side
-// overlap one's small levels with the other's work (K24 bench batch: 2.24 ->
-// 1.92 ms wall in the first A/B).  Same per-root results: each root is one
-// unchanged single-traversal run.  ABFS_BATCH_SPLIT=1 disables.
+// overlap one's small levels with the other's work.  Throughput, not
+// latency: each BFS takes longer on its share of the grid (the per-root
+// t_bfs grows), the batch finishes sooner.  Same per-root results: each root
+// is one unchanged single-traversal run.  ABFS_BATCH_SPLIT=S sets the ways
+// (1 disables).
 static int batch_ways(const abfs_traversal *t, size_t nroots) {
     if (t->is_sub || t->instrument || nroots < 2) return 1;
-    const int s = (int)env_u64("ABFS_BATCH_SPLIT", 2);
+    if (t->batch_ways_req > 0) return std::min({t->batch_ways_req, kMaxSplit, (int)nroots});
+    // measured on B200, 8-root batches: K24 1 / 2 / 4 / 8 ways 906 / 1069 / 1136 /
+    // 1022 GTEPS, ER-32M (2^25 vertices) 986 / 1103 / 1105-1178, K26 (2^26)
+    // 1251 / 1289 / 1187 (bigger levels, less to overlap), mesh 4096^2 (pure
+    // latency: every level is a cluster-solo chain) 0.91 / 1.78 / 3.4 / 6.8
+    const int def = t->max_out_degree <= 8 ? 8 : t->g->d.n > (1ull << 25) ? 2 : 4;
+    const int s = (int)env_u64("ABFS_BATCH_SPLIT", def);
     return std::max(1, std::min({s, kMaxSplit, (int)nroots}));
 }
 

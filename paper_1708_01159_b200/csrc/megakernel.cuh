@@ -132,7 +132,7 @@ int mega_launch_plain(const MegaParams &P, cudaStream_t s, int device);
 std::mutex &mega_mutex(int device);   // held from a megakernel launch to its completion
 
 constexpr uint32_t kMegaCapPart = 1u << 16;   // level records of a partition's loop
-constexpr int kMaxSplit = 4;          // batch: concurrent sub-traversals at most
+constexpr int kMaxSplit = 8;          // batch: concurrent sub-traversals at most
 constexpr uint32_t kSoloUnits = 16;   // more CTA units than this: hand the level to the grid
 
 

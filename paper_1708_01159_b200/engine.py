@@ -311,6 +311,17 @@ class Traversal:
         L.check(L.lib().abfs_traversal_set_mode(self._h, int(on)), "set_mode")
         self.mode = int(on)
 
+    def set_batch_ways(self, ways: int = 0):
+        """Fix adaptive_batch's split (1 = one full-grid launch; 0 = automatic)."""
+        L.check(L.lib().abfs_traversal_set_batch_ways(self._h, int(ways)), "set_batch_ways")
+
+    def batch_ways(self, nroots: int) -> int:
+        """Concurrent launches adaptive_batch splits nroots roots into."""
+        v = ctypes.c_int()
+        L.check(L.lib().abfs_traversal_batch_ways(self._h, int(nroots), ctypes.byref(v)),
+                "batch_ways")
+        return v.value
+
     def launches(self) -> int:
         v = ctypes.c_uint64()
         L.check(L.lib().abfs_traversal_launches(self._h, ctypes.byref(v)), "launches")
