@@ -715,7 +715,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
         // are all co-resident (cooperative)
         if (want_solo) {
             // (a refused 16-CTA cluster falls back to 8)
-            for (int cl = solo_cl; cl >= 8 && !t->mega_cluster; cl /= 2) {
+            for (int cl = solo_cl; cl >= 2 && !t->mega_cluster; cl = cl > 8 ? cl / 2 : 0) {
                 cudaLaunchConfig_t cfg = {};
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
