@@ -36,6 +36,10 @@ namespace abfs {
 // (partition.cu, megakernel.cuh): every rank adds 1 to `arrive` per level
 // (after its bitmap stores are visible system-wide) and writes its level
 // count into counts[parity][rank].
+// A rank's mailbox allocation also holds its LL receive planes (2 parities
+// x words x 8 bytes) at kLLOffset: a peer stores (epoch << 32 | word) there
+// with one 8-byte store (single-copy atomic), so the receiver needs no fence.
+constexpr size_t kLLOffset = 4096;
 struct PeerBox {
     unsigned long long arrive;
     unsigned long long mk_arrive;     // megakernel exchanges: 2^32 per rank per exchange

@@ -87,7 +87,8 @@ struct MegaParams {
     PeerBox *box;
     uint32_t nranks, rank;
     unsigned long long xseq0;   // megakernel exchanges completed before this launch (PeerBox::mk_*)
-    int xsys;                   // a peer is on another GPU: system-scope exchange signalling
+    int xsys;                   // exchange signalling: 0 GPU-scope release/acquire (same device),
+                                // 1 system-scope release/acquire, 2 LL words (cross-device)
     // optional [nroots]: per-root depth checksum (depth_mix) of the final
     // depth array of each traversal, for batch parity checks
     unsigned long long *checksums;
@@ -685,73 +686,124 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
             const uint64_t nt = (uint64_t)gridDim.x * kBlock;
             uint32_t *const *nxt_tab = P.peer_fbm + (size_t)(cur ^ 1) * P.nranks;
-            unsigned long long cnt = 0;
-            for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
-                const uint32_t v = P.visited[w];
-                const uint32_t x = v & ~P.vprev[w - P.wlo];
-                P.vprev[w - P.wlo] = v;
-                for (uint32_t r = 0; r < P.nranks; ++r) nxt_tab[r][w] = x;
-                cnt += __popc(x);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
-            if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = (unsigned)cnt;
-            __syncthreads();
-#ifdef ABFS_DIAG_PART
-            if (ABFS_DIAG_PART == 3 && lead) tdg = globaltimer();   // after the scan
-#endif
-            // one cross-rank round per level, per CTA (no grid barrier, no
-            // lead-only phase): each CTA adds its slice count into every
-            // rank's mailbox sum and releases its arrival at system scope
-            // (cumulative over the CTA's peer stores through the CTA
-            // barrier), then waits for every CTA of every rank.  A rank's CTAs
-            // add weights summing to exactly 2^32 per exchange, whatever its
-            // grid size.  The release / acquire pair is system-scoped when a
-            // peer bitmap lives on another GPU (xsys) and GPU-scoped when
-            // every rank shares this device (P = 1, ranks sharing a GPU): a
-            // system-scope release costs ~6 us per level on B200, a GPU-scope
-            // one ~1 us.  Sums rotate over 3 slots: slot (x+1)%3 is cleared
-            // by this rank before it signals exchange x, and no peer adds to
-            // it before seeing that signal.
-            if (threadIdx.x == 0) {
-                unsigned long long s = 0;
-                for (int w = 0; w < kWarps; ++w) s += warp_tot[w];
-                const uint32_t slot = (uint32_t)(xseq % 3);
-                if (lead) P.box->mk_sum[(xseq + 1) % 3] = 0;
-                const unsigned long long b = blockIdx.x, G = gridDim.x;
-                const unsigned long long wgt = ((b + 1) << 32) / G - (b << 32) / G;
-                for (uint32_t r = 0; r < P.nranks; ++r) {
-                    if (s) atomicAdd_system(&P.peer_box[r]->mk_sum[slot], s);
-                    if (P.xsys)
-                        asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
-                                     "l"(wgt) : "memory");
-                    else
-                        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
-                                     "l"(wgt) : "memory");
-                }
-                const unsigned long long expect = ((xseq + 1) * P.nranks) << 32, tw = globaltimer();
-                bool ok = true;
-                for (;;) {
-                    unsigned long long a;
-                    if (P.xsys)
-                        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
-                    else
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
-                    if (a >= expect) break;
-                    if (globaltimer() - tw > 20000000000ull) {   // a rank never arrived
-                        P.box->timeout = 1;
-                        ok = false;
-                        break;
+            if (P.xsys == 2) {
+                // LL exchange: each word goes to every rank's receive plane as
+                // one 8-byte (epoch | word) store; every rank then rebuilds
+                // its global next bitmap from its plane, spinning per word on
+                // the epoch, and counts the level from it (popc) -- no fence,
+                // one grid barrier.  Planes alternate by exchange parity: a
+                // rank writes plane x%2 again only after every rank consumed
+                // it (it waited on their exchange-(x+1) words first).
+                const unsigned long long ep = (xseq + 1) & 0xffffffffull;
+                const size_t plane = (size_t)(xseq & 1) * (P.words + 4);
+                for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
+                    const uint32_t v = P.visited[w];
+                    const uint32_t x = v & ~P.vprev[w - P.wlo];
+                    P.vprev[w - P.wlo] = v;
+                    const unsigned long long word = (ep << 32) | x;
+                    for (uint32_t r = 0; r < P.nranks; ++r) {
+                        unsigned long long *ll = reinterpret_cast<unsigned long long *>(
+                            reinterpret_cast<char *>(P.peer_box[r]) + kLLOffset) + plane;
+                        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(ll + w), "l"(word) : "memory");
                     }
-                    __nanosleep(32);
                 }
-                unsigned long long g = 0;
-                if (ok) g = *(volatile unsigned long long *)&P.box->mk_sum[slot];
-                s_nw = g;   // 0 ends the traversal
+                const unsigned long long *mine = reinterpret_cast<const unsigned long long *>(
+                    reinterpret_cast<const char *>(P.box) + kLLOffset) + plane;
+                uint32_t *const fn = cur ? P.fbm0 : P.fbm1;   // this rank's next bitmap
+                unsigned long long cnt = 0;
+                const unsigned long long tw = globaltimer();
+                bool ok = true;
+                for (uint64_t w = tid; w < P.words && ok; w += nt) {
+                    unsigned long long word;
+                    for (;;) {
+                        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(word) : "l"(mine + w) : "memory");
+                        if ((word >> 32) == ep) break;
+                        if (globaltimer() - tw > 20000000000ull) {   // a rank never sent
+                            P.box->timeout = 1;
+                            ok = false;
+                            break;
+                        }
+                    }
+                    fn[w] = (uint32_t)word;
+                    cnt += __popc((uint32_t)word);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
+                if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&P.ctr->oe3[out], cnt);
+                (void)ok;   // a timed-out CTA set box->timeout; every CTA reads it below
+                ++xseq;
+                grid.sync();
+                nw = *(volatile unsigned *)&P.box->timeout
+                         ? 0ull : *(volatile unsigned long long *)&P.ctr->oe3[out];
+            } else {
+                unsigned long long cnt = 0;
+                for (uint64_t w = P.wlo + tid; w < P.wend; w += nt) {
+                    const uint32_t v = P.visited[w];
+                    const uint32_t x = v & ~P.vprev[w - P.wlo];
+                    P.vprev[w - P.wlo] = v;
+                    for (uint32_t r = 0; r < P.nranks; ++r) nxt_tab[r][w] = x;
+                    cnt += __popc(x);
+                }
+    #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
+                if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = (unsigned)cnt;
+                __syncthreads();
+    #ifdef ABFS_DIAG_PART
+                if (ABFS_DIAG_PART == 3 && lead) tdg = globaltimer();   // after the scan
+    #endif
+                // one cross-rank round per level, per CTA (no grid barrier, no
+                // lead-only phase): each CTA adds its slice count into every
+                // rank's mailbox sum and releases its arrival at system scope
+                // (cumulative over the CTA's peer stores through the CTA
+                // barrier), then waits for every CTA of every rank.  A rank's CTAs
+                // add weights summing to exactly 2^32 per exchange, whatever its
+                // grid size.  The release / acquire pair is system-scoped when a
+                // peer bitmap lives on another GPU (xsys) and GPU-scoped when
+                // every rank shares this device (P = 1, ranks sharing a GPU): a
+                // system-scope release costs ~6 us per level on B200, a GPU-scope
+                // one ~1 us.  Sums rotate over 3 slots: slot (x+1)%3 is cleared
+                // by this rank before it signals exchange x, and no peer adds to
+                // it before seeing that signal.
+                if (threadIdx.x == 0) {
+                    unsigned long long s = 0;
+                    for (int w = 0; w < kWarps; ++w) s += warp_tot[w];
+                    const uint32_t slot = (uint32_t)(xseq % 3);
+                    if (lead) P.box->mk_sum[(xseq + 1) % 3] = 0;
+                    const unsigned long long b = blockIdx.x, G = gridDim.x;
+                    const unsigned long long wgt = ((b + 1) << 32) / G - (b << 32) / G;
+                    for (uint32_t r = 0; r < P.nranks; ++r) {
+                        if (s) atomicAdd_system(&P.peer_box[r]->mk_sum[slot], s);
+                        if (P.xsys)
+                            asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
+                                         "l"(wgt) : "memory");
+                        else
+                            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&P.peer_box[r]->mk_arrive),
+                                         "l"(wgt) : "memory");
+                    }
+                    const unsigned long long expect = ((xseq + 1) * P.nranks) << 32, tw = globaltimer();
+                    bool ok = true;
+                    for (;;) {
+                        unsigned long long a;
+                        if (P.xsys)
+                            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
+                        else
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(&P.box->mk_arrive) : "memory");
+                        if (a >= expect) break;
+                        if (globaltimer() - tw > 20000000000ull) {   // a rank never arrived
+                            P.box->timeout = 1;
+                            ok = false;
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
+                    unsigned long long g = 0;
+                    if (ok) g = *(volatile unsigned long long *)&P.box->mk_sum[slot];
+                    s_nw = g;   // 0 ends the traversal
+                }
+                ++xseq;
+                __syncthreads();
+                nw = s_nw;
             }
-            ++xseq;
-            __syncthreads();
-            nw = s_nw;
         } else {
             nw = topdown ? (unsigned long long)*(volatile unsigned *)&P.ctr->qlen[out]
                          : *(volatile unsigned long long *)&P.ctr->count[out];

@@ -73,7 +73,7 @@ struct abfs_part {
     std::vector<void *> ipc_opened;              // peer allocations mapped by IPC
     // persistent per-rank level loop (abfs_part_mega_*)
     uint32_t *q2 = nullptr;                      // second global-size queue
-    MegaRecord *mrecs = nullptr, *drecs = nullptr;
+    MegaRecord *mrecs = nullptr, *drecs = nullptr;   // host staging / device records
     unsigned long long *mnlev = nullptr, *dnlev = nullptr;
     uint32_t *droots = nullptr;
     unsigned char *dtree = nullptr;
@@ -288,6 +288,7 @@ extern "C" void abfs_part_destroy(abfs_part *p) {
     cudaFree(p->box);
     cudaFree(p->q2);
     if (p->mrecs) cudaFreeHost(p->mrecs);
+    cudaFree(p->drecs);
     if (p->mnlev) cudaFreeHost(p->mnlev);
     cudaFree(p->droots);
     cudaFree(p->dtree);
@@ -325,9 +326,11 @@ static int part_alloc_state(abfs_part *p) {
     A((void **)&p->dctr, sizeof(Ctr));
     A((void **)&p->dmb, sizeof(Mailbox));
     A((void **)&p->dres, 2 * sizeof(unsigned long long));
-    A((void **)&p->box, sizeof(PeerBox));
+    static_assert(sizeof(PeerBox) <= kLLOffset, "LL planes overlap the mailbox");
+    const size_t box_bytes = kLLOffset + 2 * (p->W + 4) * sizeof(unsigned long long);
+    A((void **)&p->box, box_bytes);
     A((void **)&p->pack_ticket, sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemsetAsync(p->box, 0, sizeof(PeerBox), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->box, 0, box_bytes, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->pack_ticket, 0, sizeof(unsigned int), s);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&p->hres, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(p->dctr, 0, sizeof(Ctr), s);
@@ -935,8 +938,11 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     cudaStream_t s = p->stream;
     if (!p->mrecs) {
         ABFS_CUDA(cudaMalloc(&p->q2, (p->n + 4) * 4));
-        ABFS_CUDA(cudaHostAlloc((void **)&p->mrecs, kMegaCapPart * sizeof(MegaRecord), cudaHostAllocMapped));
-        ABFS_CUDA(cudaHostGetDevicePointer((void **)&p->drecs, p->mrecs, 0));
+        // records in device memory, copied back after the launch: a level's
+        // system-scope exchange release would otherwise wait on the lead's
+        // PCIe record writes to mapped host memory
+        ABFS_CUDA(cudaMallocHost((void **)&p->mrecs, kMegaCapPart * sizeof(MegaRecord)));
+        ABFS_CUDA(cudaMalloc((void **)&p->drecs, kMegaCapPart * sizeof(MegaRecord)));
         ABFS_CUDA(cudaHostAlloc((void **)&p->mnlev, sizeof(unsigned long long), cudaHostAllocMapped));
         ABFS_CUDA(cudaHostGetDevicePointer((void **)&p->dnlev, p->mnlev, 0));
         ABFS_CUDA(cudaMalloc(&p->droots, 16));
@@ -1005,8 +1011,11 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     P.rank = p->rank;
     P.xseq0 = p->mk_seq;
     {
-        const char *xs = getenv("ABFS_XSYS");   // tests: force system-scope signalling
-        P.xsys = xs ? (atoi(xs) != 0) : p->x_sys;
+        // cross-device ranks: LL exchange (no system-scope fence per level);
+        // same device: GPU-scoped release / acquire.  ABFS_XSYS=0/1/2 forces
+        // GPU scope / system scope / LL (tests)
+        const char *xs = getenv("ABFS_XSYS");
+        P.xsys = xs ? atoi(xs) : (p->x_sys ? 2 : 0);
     }
     P.checksums = nullptr;
     P.acc = nullptr;   // RED-mode levels are single-graph only
@@ -1021,6 +1030,9 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     }
     const unsigned long long nl = *(volatile unsigned long long *)p->mnlev;
     p->mk_seq += nl;
+    ABFS_CUDA(cudaMemcpy(p->mrecs, p->drecs,
+                         (size_t)std::min<unsigned long long>(nl, kMegaCapPart) * sizeof(MegaRecord),
+                         cudaMemcpyDeviceToHost));
     p->last_kernel = -1;
     p->has_q = false;
     int timed_out = 0;

@@ -93,11 +93,13 @@ def test_partitions_equal_single_gpu_engine(cfg, parts, exchange):
             np.testing.assert_array_equal(bfs.depths(), want)
 
 
-@pytest.mark.parametrize("xsys", ["0", "1"])
+@pytest.mark.parametrize("xsys", ["0", "1", "2"])
 def test_persistent_partition_loop_exchange_scopes(xsys, monkeypatch):
-    """The persistent per-rank loop signals each exchange at GPU scope when
-    every peer bitmap is on this device and at system scope otherwise
-    (ABFS_XSYS forces either); both must give the single-engine traversal."""
+    """The persistent per-rank loop's exchange: GPU-scoped release/acquire when
+    every peer bitmap is on this device (0), system-scoped (1), or the LL
+    words (epoch | bitmap word in one 8-byte store, no fence) used across
+    devices (2); ABFS_XSYS forces each; all must give the single-engine
+    traversal."""
     monkeypatch.setenv("ABFS_XSYS", xsys)
     dg = DeviceGraph.rmat(18, 16 << 18, 1, symmetrize=True)
     stats = P.compute_stats(dg)
