@@ -149,6 +149,7 @@ static int64_t vw_chunk(const abfs_traversal *t, int64_t chunk) {
     }
     const int64_t cap = (int64_t)env_u64("ABFS_VW_MAX", 32);
     if (w > cap) w = cap;
+    if (const uint64_t f = env_u64("ABFS_VW_FORCE", 0)) w = (int64_t)f;   // A/B experiments
     return chunk < w ? chunk : w;
 }
 
@@ -798,6 +799,11 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     {
         const int64_t vc = vw_chunk(t, chunk);
         P.vw_log2 = vc >= 32 ? 5 : vc >= 16 ? 4 : vc >= 8 ? 3 : vc >= 4 ? 2 : vc >= 2 ? 1 : 0;
+        const int64_t wc = chunk < 32 ? chunk : 32;
+        P.vw_wide_log2 = wc >= 32 ? 5 : wc >= 16 ? 4 : wc >= 8 ? 3 : wc >= 4 ? 2 : wc >= 2 ? 1 : 0;
+        if (env_u64("ABFS_VW_FORCE", 0)) P.vw_wide_log2 = P.vw_log2;   // A/B: one width for all levels
+        // ER-32M, F <= 28 K levels: 21.8 -> 10.5 us (F = 877), 49 -> 39 us (F = 28 K)
+        P.vw_wide_f = env_u64("ABFS_VW_WIDE_F", 1ull << 16);
     }
     P.instrument = t->instrument ? 1 : 0;
     P.pull_light = pull_light();

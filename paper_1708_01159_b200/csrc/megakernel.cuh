@@ -52,6 +52,11 @@ struct MegaParams {
     uint32_t tree_nodes;
     int fixed_pair;      // >= 0: bfs_full with this pair ordinal, no tree
     int vw_log2;
+    // push-warp levels with at most vw_wide_f frontier vertices run at width
+    // 2^vw_wide_log2 (= min(chunk, 32)) instead of the degree-fitted one: a
+    // small level's chain is shorter with more lanes per vertex
+    int vw_wide_log2;
+    unsigned long long vw_wide_f;
     int instrument;
     uint32_t pull_light;
     uint32_t cap;
@@ -245,7 +250,9 @@ __device__ __forceinline__ int mega_strategy(const MegaParams &P, const LevelCtx
     case 2:
     case 4: {
         if (kernel == 2) push_body<VAR>(c, sq, q, F, P.out_off, P.dst, blockIdx.x, gridDim.x);
-        else push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst, P.vw_log2, blockIdx.x, gridDim.x);
+        else push_warp_body<VAR>(c, sq, q, F, P.out_off, P.dst,
+                                 F <= P.vw_wide_f && P.vw_wide_log2 > P.vw_log2 ? P.vw_wide_log2 : P.vw_log2,
+                                 blockIdx.x, gridDim.x);
         ABFS_DIAG_MARK(0);
         grid.sync();
         const unsigned nu = units();

@@ -986,6 +986,8 @@ static int part_mega(abfs_part *p, int64_t root, const abfs_tree *tr, const doub
     P.tree_nodes = nn;
     P.fixed_pair = fixed_pair;
     P.vw_log2 = chunk >= 32 ? 5 : chunk >= 16 ? 4 : chunk >= 8 ? 3 : chunk >= 4 ? 2 : chunk >= 2 ? 1 : 0;
+    P.vw_wide_log2 = P.vw_log2;
+    P.vw_wide_f = 0;
     P.instrument = 0;
     P.pull_light = kPullLight;
     P.cap = kMegaCapPart;
