@@ -665,10 +665,6 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         }
         const unsigned long long settled = discovered + P.n_noin;
         const bool wide = P.pull_wide_max && (settled >= P.n || P.n - settled <= P.pull_wide_max);
-#ifdef ABFS_DIAG_PART
-        unsigned long long tdg = 0;
-        if (ABFS_DIAG_PART == 1 && lead) tdg = globaltimer();   // after conversions
-#endif
         int sflags;
         switch (pv) {
         case 0: sflags = mega_strategy<0>(P, c, pk, (uint32_t)frontier, q_cur, pull_next, &sq, &sn, &s_done, pfound, s_fetch, warp_tot, &s_base, wide, use_pl ? &pl : nullptr, pl_n, grid); break;
@@ -683,9 +679,6 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             pl_have = -1;
         }
         unsigned long long nw;
-#ifdef ABFS_DIAG_PART
-        if (ABFS_DIAG_PART == 2 && lead) tdg = globaltimer();   // after the strategy
-#endif
         if (PART) {
             // fused frontier exchange: the visited bits this rank gained are
             // stored into every rank's next-frontier bitmap over peer memory,
@@ -751,24 +744,20 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                     for (uint32_t r = 0; r < P.nranks; ++r) nxt_tab[r][w] = x;
                     cnt += __popc(x);
                 }
-    #pragma unroll
+#pragma unroll
                 for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
                 if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = (unsigned)cnt;
                 __syncthreads();
-    #ifdef ABFS_DIAG_PART
-                if (ABFS_DIAG_PART == 3 && lead) tdg = globaltimer();   // after the scan
-    #endif
                 // one cross-rank round per level, per CTA (no grid barrier, no
                 // lead-only phase): each CTA adds its slice count into every
                 // rank's mailbox sum and releases its arrival at system scope
                 // (cumulative over the CTA's peer stores through the CTA
                 // barrier), then waits for every CTA of every rank.  A rank's CTAs
                 // add weights summing to exactly 2^32 per exchange, whatever its
-                // grid size.  The release / acquire pair is system-scoped when a
-                // peer bitmap lives on another GPU (xsys) and GPU-scoped when
-                // every rank shares this device (P = 1, ranks sharing a GPU): a
-                // system-scope release costs ~6 us per level on B200, a GPU-scope
-                // one ~1 us.  Sums rotate over 3 slots: slot (x+1)%3 is cleared
+                // grid size.  GPU-scoped when every rank shares this device
+                // (P = 1, ranks sharing a GPU: ~1 us); system-scoped only when
+                // forced (ABFS_XSYS=1: ~6 us per level on B200, which is why
+                // cross-device ranks take the LL branch above).  Sums rotate over 3 slots: slot (x+1)%3 is cleared
                 // by this rank before it signals exchange x, and no peer adds to
                 // it before seeing that signal.
                 if (threadIdx.x == 0) {
@@ -856,11 +845,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             r.frontier = frontier;
             r.new_count = nw;
             r.t_start = t0;
-#ifdef ABFS_DIAG_PART
-            r.t_pred = tdg;
-#else
             r.t_pred = tp;
-#endif
             r.t_end = globaltimer();
             // partitions: this rank's count through the level's count variant
             r.next_out_edges = next_oe;
