@@ -131,10 +131,14 @@ def test_partition_rejects_misaligned_range():
         DevicePartition(dg, 0, n + 1)
 
 
-def test_peer_exchange_over_cuda_ipc_two_processes():
+@pytest.mark.parametrize("xsys", [None, "2"])
+def test_peer_exchange_over_cuda_ipc_two_processes(xsys, monkeypatch):
     """DistPeerExchange: two processes (one GPU here; one per GPU in
     production) map each other's bitmaps/mailboxes by CUDA IPC and exchange
-    frontier slices with the fused peer-store kernel."""
+    frontier slices with the fused peer-store kernel (xsys "2": the LL-word
+    exchange cross-device ranks use, forced on the shared GPU)."""
+    if xsys is not None:
+        monkeypatch.setenv("ABFS_XSYS", xsys)
     import sys
     sys.path.insert(0, ROOT)
     from tools import ipc_two_ranks
