@@ -340,6 +340,10 @@ __device__ __forceinline__ bool solo_fits(const MegaParams &P, int kernel,
     return false;
 }
 
+#ifndef ABFS_SOLO_DSMEM
+#define ABFS_SOLO_DSMEM 1
+#endif
+
 #ifndef ABFS_MEGA_MINB
 #define ABFS_MEGA_MINB 5
 #endif
@@ -360,6 +364,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned s_base;
     __shared__ unsigned long long s_nw;   // partition mode: the exchanged level count
+    __shared__ unsigned s_solo_cnt[3][2]; // solo mode: cluster 0's queue / unit tails
+                                          // (CTA 0's copy, reached over DSMEM), rotating slots
     __shared__ __align__(16) CutNode s_tree[kMegaTreeNodes];
     cg::grid_group grid = cg::this_grid();
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -457,12 +463,22 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
             // ~0.3 us) while every other CTA waits at ONE grid barrier
             if (blockIdx.x < P.solo_ctas) {
                 cg::cluster_group cl = cg::this_cluster();
+                // the level counters live in CTA 0's shared memory: the
+                // cluster's tail atomics and the count readback are DSMEM
+                // round trips instead of L2 ones
+                unsigned *const cnt0 = ABFS_SOLO_DSMEM ? cl.map_shared_rank(&s_solo_cnt[0][0], 0) : nullptr;
+                if (ABFS_SOLO_DSMEM) {
+                    if (lead)
+                        for (int s = 0; s < 3; ++s) s_solo_cnt[s][0] = s_solo_cnt[s][1] = 0;
+                    cl.sync();
+                }
                 uint32_t L = level;
                 int fb = fallback;
                 unsigned long long ts = t0, tq = tp;
                 int ppk = pk, ppv = pv;   // pair of the last executed level
                 for (;;) {
                     const int o = (int)(L % 3), z = (int)((L + 1) % 3);
+                    if (ABFS_SOLO_DSMEM && lead) s_solo_cnt[z][0] = s_solo_cnt[z][1] = 0;
                     if (lead && L != level) {
                         P.ctr->qlen[z] = 0;
                         P.ctr->units[z] = 0;
@@ -480,9 +496,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                     sc.visited = P.visited;
                     sc.fbm = cur ? P.fbm1 : P.fbm0;
                     sc.q_next = cur ? P.q0 : P.q1;
-                    sc.q_tail = &P.ctr->qlen[o];
+                    sc.q_tail = ABFS_SOLO_DSMEM ? cnt0 + 2 * o : &P.ctr->qlen[o];
                     sc.count = &P.ctr->count[o];
-                    sc.units_tail = &P.ctr->units[o];
+                    sc.units_tail = ABFS_SOLO_DSMEM ? cnt0 + 2 * o + 1 : &P.ctr->units[o];
                     sc.units = P.units;
                     sc.inconsistent = &P.ctr->inconsistent;
                     sc.ctr = P.ctr;
@@ -507,6 +523,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                         // claims so far stay counted in qlen[o]; units are rebuilt)
                         if (lead) {
                             P.ctr->units[o] = 0;
+                            // the claims taken so far stay counted (the grid
+                            // continues the global tail)
+                            if (ABFS_SOLO_DSMEM) P.ctr->qlen[o] = s_solo_cnt[o][0];
                             P.solo->level = L;
                             P.solo->frontier = frontier;
                             P.solo->discovered = discovered;
