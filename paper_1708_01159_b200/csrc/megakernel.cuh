@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
     __shared__ unsigned warp_tot[kWarps];
     __shared__ unsigned s_base;
     __shared__ unsigned long long s_nw;   // partition mode: the exchanged level count
+    __shared__ unsigned s_incons;         // ctr->inconsistent, constant for a traversal
     __shared__ unsigned s_solo_cnt[3][2]; // solo mode: cluster 0's queue / unit tails
                                           // (CTA 0's copy, reached over DSMEM), rotating slots
     __shared__ __align__(16) CutNode s_tree[kMegaTreeNodes];
@@ -424,6 +425,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         }
         grid.sync();
     }
+    // the run_level-contract flag is fixed for the whole traversal (set by the
+    // host's prepare or by the init above): every level's claims read a
+    // shared-memory copy instead of an L2 round trip
+    if (threadIdx.x == 0) s_incons = *(volatile unsigned *)&P.ctr->inconsistent;
+    __syncthreads();
     unsigned long long frontier = 1, discovered = 1;
     int pk = 0, pv = 0;   // DEFAULT_KERNEL (adaptive.py:36-38)
     int cur = 0;
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                     sc.count = &P.ctr->count[o];
                     sc.units_tail = ABFS_SOLO_DSMEM ? cnt0 + 2 * o + 1 : &P.ctr->units[o];
                     sc.units = P.units;
-                    sc.inconsistent = &P.ctr->inconsistent;
+                    sc.inconsistent = &s_incons;
                     sc.ctr = P.ctr;
                     sc.mb = nullptr;
                     sc.es = nullptr;
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.count = &P.ctr->count[out];
         c.units_tail = &P.ctr->units[out];
         c.units = P.units;
-        c.inconsistent = &P.ctr->inconsistent;
+        c.inconsistent = &s_incons;
         c.ctr = P.ctr;
         c.mb = nullptr;
         c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
