@@ -95,6 +95,7 @@ struct LevelCtx {
     unsigned long long *es;      // optional: in-edges scanned by pull (instrumented runs)
     unsigned long long *work;    // dynamic work cursor of this level (= &ctr->work[out])
     uint32_t pull_light;         // pull phase A: entries each lane scans alone
+    uint32_t direct_claim;       // claim4: no visited-word filter load before the atomic
     uint32_t *acc;               // non-null: RED-mode top-down claims (candidate bits are
                                  // OR-ed here fire-and-forget; red_compact_body settles them)
     unsigned long long seq;
@@ -203,7 +204,8 @@ __device__ __forceinline__ void claim4(const LevelCtx &c, const uint32_t (&v)[4]
     }
     uint32_t wv[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) wv[k] = act[k] ? c.visited[v[k] >> 5] : 0xffffffffu;
+    for (int k = 0; k < 4; ++k)
+        wv[k] = !act[k] ? 0xffffffffu : c.direct_claim ? 0u : c.visited[v[k] >> 5];
     if (c.acc) {
         // RED mode: no returning atomic, no depth write, no emission here --
         // the unvisited candidates' bits go to acc with fire-and-forget

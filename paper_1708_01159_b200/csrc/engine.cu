@@ -267,6 +267,7 @@ static int level_impl(abfs_traversal *t, int64_t level, int kernel, int variant,
     c.es = nullptr;
     c.work = &t->dctr->work[out];
     c.pull_light = pull_light();
+    c.direct_claim = 0;
     if (t->instrument) {
         ABFS_CUDA(cudaMemsetAsync(t->des, 0, sizeof(unsigned long long), s));
         c.es = t->des;
@@ -816,6 +817,11 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.solo_ctas = t->mega_cluster ? (uint32_t)t->mega_cluster : 0u;
     P.solo = t->dsolo;
     P.solo_passes = (uint32_t)env_u64("ABFS_SOLO_PASSES", 2);   // mesh 4096^2: 2 passes -9 % vs 1
+    // claims without the visited-word filter load: every solo level (mesh
+    // 4096^2 -8.5 %: the filter load is one more L2 round trip on a level's
+    // chain) and grid levels of at most direct_f frontier vertices
+    P.solo_direct = (uint32_t)env_u64("ABFS_SOLO_DIRECT", 1);
+    P.direct_f = env_u64("ABFS_DIRECT_F", 0);
     P.part = 0;
     P.m_rev = g.m;
     P.lo = 0;

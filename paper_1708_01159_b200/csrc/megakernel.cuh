@@ -73,6 +73,8 @@ struct MegaParams {
     // barriers) while the other CTAs wait at one grid barrier
     uint32_t solo_ctas;
     uint32_t solo_passes;       // frontier passes of the cluster's threads a solo level may take
+    uint32_t solo_direct;       // solo levels claim without the visited-word filter load
+    unsigned long long direct_f; // grid top-down levels of at most this many frontier vertices too
     struct SoloState *solo;
     // ---- vertex partition (part = 1; partition.cu): this rank owns
     // destinations [lo, hi); depth / visited / noin / in_off / first_src are
@@ -512,6 +514,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
                     sc.es = nullptr;
                     sc.work = &P.ctr->work[o];
                     sc.pull_light = P.pull_light;
+                    sc.direct_claim = P.solo_direct;
                     sc.seq = 0;
                     sc.zero_slot = z;
                     sc.level = (int32_t)L;
@@ -669,6 +672,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         c.es = P.instrument ? &P.ctr->es3[out] : nullptr;
         c.work = &P.ctr->work[out];
         c.pull_light = P.pull_light;
+        c.direct_claim = frontier <= P.direct_f ? 1u : 0u;
         // RED-mode top-down level (single graph, big frontier): the same for
         // every CTA (depends on the level's pair and frontier only)
         c.acc = (need_queue && P.acc && frontier >= P.red_frontier) ? P.acc : nullptr;

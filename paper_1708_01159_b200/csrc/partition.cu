@@ -571,6 +571,7 @@ static int part_strategy(abfs_part *p, int64_t level, int kernel, int variant, i
     c.es = nullptr;
     c.work = &p->dctr->work[out];
     c.pull_light = kPullLight;
+    c.direct_claim = 0;
     c.seq = seq;
     c.zero_slot = (int)(seq % 3);
     c.level = (int32_t)level;
