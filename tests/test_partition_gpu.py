@@ -207,15 +207,20 @@ def test_generated_partitions_bfs_equal_single_gpu_engine():
         np.testing.assert_array_equal(bfs.depths(), want)
 
 
-def test_multi_gpu_bench_runs_end_to_end_with_ranks_sharing_one_gpu():
+@pytest.mark.parametrize("xsys", [None, "2"])
+def test_multi_gpu_bench_runs_end_to_end_with_ranks_sharing_one_gpu(xsys, monkeypatch):
     """bench.py --gpus 2 under torchrun (the driver's SCALE launch) with both
     ranks on GPU 0 (--shared-gpu: gloo control plane; slices from the
-    generator stream; fused peer exchange over CUDA IPC): one JSON line."""
+    generator stream; fused peer exchange over CUDA IPC): one JSON line
+    (xsys "2": with the cross-device LL-word exchange forced)."""
+    if xsys is not None:
+        monkeypatch.setenv("ABFS_XSYS", xsys)
     import json
     import subprocess
     import sys
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29533 + (xsys is not None)),
+           "bench.py", "--gpus", "2",
            "--shared-gpu", "--scale", "14", "--steps", "1", "--warmup", "3",
            "--roots-per-step", "2"]
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
