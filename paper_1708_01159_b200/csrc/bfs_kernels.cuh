@@ -119,7 +119,11 @@ constexpr int kQBuf = ABFS_QBUF;      // TWO_LEVEL CTA-local queue buffer (also 
 constexpr int kEdgeTileMax = kBlock * 4 * 4;  // edge slots per CTA iteration (4 x uint4 / thread)
 constexpr uint32_t kHeavy = 256;      // push-warp: degree above -> CTA units
 constexpr uint32_t kUnit = 1024;      // edges per CTA work unit (4 steps of 256)
-constexpr uint32_t kPushHub = 64;     // vertex push: degree above -> CTA units
+#ifndef ABFS_PUSH_HUB
+#define ABFS_PUSH_HUB 64
+#endif
+constexpr uint32_t kPushHub = ABFS_PUSH_HUB;   // vertex push: degree above -> CTA units
+constexpr uint64_t kSoloMaxDegree = 64;        // cluster solo mode: graphs of max out-degree <= this
 constexpr uint32_t kPullLight = 32;   // pull phase A default (ABFS_PULL_LIGHT overrides)
 #ifndef ABFS_PULL_HEAVY
 #define ABFS_PULL_HEAVY 256

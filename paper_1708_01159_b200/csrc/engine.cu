@@ -686,7 +686,7 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     // Kronecker-24).  The kernel without solo code spills less (224 / 340 B
     // instead of 260 / 504 B).
     const char *solo_env = getenv("ABFS_SOLO");
-    const bool want_solo = solo_env ? atoi(solo_env) != 0 : t->max_out_degree <= kPushHub;
+    const bool want_solo = solo_env ? atoi(solo_env) != 0 : t->max_out_degree <= kSoloMaxDegree;
 #ifdef ABFS_MEGA_VARIANTS   // occupancy experiments (set_mode 2 / 3)
     void *kfn = t->mega_minb == 4   ? (void *)k_mega<4, false>
                 : t->mega_minb == 6 ? (void *)k_mega<6, false>
