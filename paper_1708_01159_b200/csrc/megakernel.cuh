@@ -75,6 +75,7 @@ struct MegaParams {
     uint32_t solo_passes;       // frontier passes of the cluster's threads a solo level may take
     uint32_t solo_direct;       // solo levels claim without the visited-word filter load
     unsigned long long direct_f; // grid top-down levels of at most this many frontier vertices too
+    uint32_t red_direct;         // RED-mode levels reduce every candidate (no filter load)
     struct SoloState *solo;
     // ---- vertex partition (part = 1; partition.cu): this rank owns
     // destinations [lo, hi); depth / visited / noin / in_off / first_src are
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         // RED-mode top-down level (single graph, big frontier): the same for
         // every CTA (depends on the level's pair and frontier only)
         c.acc = (need_queue && P.acc && frontier >= P.red_frontier) ? P.acc : nullptr;
+        if (c.acc && P.red_direct) c.direct_claim = 1u;
         c.seq = 0;
         c.zero_slot = zero;
         c.level = (int32_t)level;
