@@ -823,9 +823,15 @@ static int mega_run(abfs_traversal *t, const uint32_t *roots, size_t nroots, boo
     P.solo_direct = (uint32_t)env_u64("ABFS_SOLO_DIRECT", 1);
     P.direct_f = env_u64("ABFS_DIRECT_F", 0);
     // RED levels reduce every candidate without the visited-word filter load
-    // (ER-32M BFS -8.6 %: its 883 K-vertex push level reaches mostly unvisited
-    // vertices, so the filter only lengthened the chain; K24 / K26 +-0.3 %)
-    P.red_direct = (uint32_t)env_u64("ABFS_RED_DIRECT", 1);
+    // on graphs without a heavy tail (max out-degree <= 4 x mean; ER-32M BFS
+    // -8.6 %: its 883 K-vertex push level reaches mostly unvisited vertices,
+    // so the filter only lengthened the chain).  Hub frontiers keep the
+    // filter: their neighbourhoods overlap, and the unfiltered duplicates
+    // cost fixed-push K24 runs 1.5x.
+    {
+        const uint64_t mean = g.n ? g.m / g.n : 0;
+        P.red_direct = (uint32_t)env_u64("ABFS_RED_DIRECT", t->max_out_degree <= 4 * (mean ? mean : 1));
+    }
     P.part = 0;
     P.m_rev = g.m;
     P.lo = 0;

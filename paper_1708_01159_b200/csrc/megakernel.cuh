@@ -677,7 +677,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mega(MegaParams P) {
         // RED-mode top-down level (single graph, big frontier): the same for
         // every CTA (depends on the level's pair and frontier only)
         c.acc = (need_queue && P.acc && frontier >= P.red_frontier) ? P.acc : nullptr;
-        if (c.acc && P.red_direct) c.direct_claim = 1u;
+        // unfiltered RED only while most vertices are unvisited (the filter
+        // load would mostly pass); late top-down levels keep it
+        if (c.acc && P.red_direct && (P.n - discovered) * 2 > P.n) c.direct_claim = 1u;
         c.seq = 0;
         c.zero_slot = zero;
         c.level = (int32_t)level;
