@@ -517,6 +517,42 @@ def test_red_mode_all_pairs_and_traces_match_reference(name, red_mode):
             np.testing.assert_array_equal(d, want)
 
 
+@pytest.fixture(params=[("1", "8", "1"), ("1", "16", "1"), ("1", "16", "0"), ("1", "4", "1")],
+                ids=["solo8", "solo16", "solo16-filtered", "solo4"])
+def solo_forced(request, monkeypatch):
+    """Force the megakernel's cluster solo mode (small top-down levels on one
+    cluster with DSMEM tails) on every graph, hubs included: solo levels that
+    meet a hub hand the level back to the grid mid-flight."""
+    on, cl, direct = request.param
+    monkeypatch.setenv("ABFS_SOLO", on)
+    monkeypatch.setenv("ABFS_SOLO_CLUSTER", cl)
+    monkeypatch.setenv("ABFS_SOLO_DIRECT", direct)
+    yield request.param
+
+
+@pytest.mark.parametrize("name", ["kron10", "kron12", "star7", "u1000", "mesh64", "unreach", "hand1"])
+def test_forced_solo_mode_all_pairs_and_traces_match_reference(name, solo_forced):
+    g = graph(name)
+    t = g.device_graph().scratch()
+    assert t.mode
+    stats = P.compute_stats(g)
+    traces = G.traces()["small"]
+    for r in G.roots(name):
+        want = G.depth(name, r)
+        cnt = G.counts(name, r).tolist()
+        for k, v in P.ALL_PAIRS:
+            if k in (P.KernelId.VERTEX_PUSH, P.KernelId.VERTEX_PUSH_WARP):   # solo-eligible
+                d, outs = P.bfs_full(g, r, k, v)
+                np.testing.assert_array_equal(d, want, err_msg=f"{name} root={r} {k.name} {v.name}")
+                assert [o.new_frontier_count for o in outs] == cnt, (name, r, k, v)
+        for key, tree in G.trees_for(name):
+            d, tr = P.adaptive_bfs(g, r, P.deserialize(G.tree_path(tree)), stats)
+            got = [[int(x.kernel), int(x.variant), int(x.fallback_used), x.frontier_size]
+                   for x in tr.records]
+            assert got == traces[name][str(r)][key], (name, r, key)
+            np.testing.assert_array_equal(d, want)
+
+
 def test_red_mode_batch_checksums_k18(red_mode):
     """RED mode through the batched launch the bench times: per-root depth
     checksums and per-level counts equal the oracle's on Kronecker-18."""
