@@ -789,7 +789,9 @@ def run_multi(a):
                        "model": os.path.relpath(a.model, ROOT),
                        "l2": "inputs larger than L2"},
             "gpu_launches": int(launches),
-            "exchange": {"kind": "fused peer stores over NVLink (CUDA IPC) + mailbox arrival counters",
+            "exchange": {"kind": "fused peer stores over NVLink (CUDA IPC) inside the per-rank megakernel: "
+                                 "LL words (epoch | bitmap word, one 8-byte store, no fence) between "
+                                 "devices, GPU-scoped release/acquire arrival counters on one device",
                          "bytes_received_per_rank_per_level": recv,
                          "levels_timed": nlev,
                          "nvlink_peak_GBps_per_direction": 900.0,
