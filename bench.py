@@ -783,8 +783,8 @@ def run_multi(a):
                        "step": f"{R} tree-switched BFSs, one at a time over all ranks (one "
                                "persistent per-rank launch each)",
                        "parallelism": f"1-D edge-balanced destination partition, {world} ranks x 1 GPU; "
-                                      "per-level frontier exchange = fused NVLink peer stores + "
-                                      "mailbox signal inside the per-rank megakernel",
+                                      "per-level frontier exchange = fused NVLink peer stores "
+                                      "inside the per-rank megakernel (LL words across devices)",
                        "slices": "built per rank from the generator stream (whole graph never resident)",
                        "model": os.path.relpath(a.model, ROOT),
                        "l2": "inputs larger than L2"},
