@@ -302,6 +302,11 @@ def test_split_batch_equals_one_launch(name, monkeypatch):
             np.testing.assert_array_equal(t.read(), G.depth(name, batch[-1]))
         lv, ns, tot = t.adaptive_batch(order, flat.as_abfs(), st)
         assert (ns > 0).all() and tot > 0 and lv.tolist() == base[len(order)][0]
+        assert t.batch_ways(len(order)) == min(int(ways), len(order)) and t.batch_ways(1) == 1
+        t.set_batch_ways(1)   # the explicit setting wins over ABFS_BATCH_SPLIT
+        assert t.batch_ways(len(order)) == 1
+        with pytest.raises(Exception):
+            t.set_batch_ways(-1)
         t.close()
     dg.close()
 
